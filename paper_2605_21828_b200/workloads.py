@@ -1,0 +1,75 @@
+"""Workload -> (basis, trees) -> plan file.  Host precompute, outside the timed path.
+
+Geometry, modes and coefficient vectors come from ``mht_inputs`` (the seeded
+generators shared with the oracle); the butterfly factorization is built here.
+"""
+from __future__ import annotations
+
+import dataclasses
+import os
+
+import numpy as np
+
+import mht_inputs as mi
+
+from .precompute.basis import DenseBasis, FlatBasis, SphereBasis
+from .precompute.builder import build_plan
+from .precompute.trees import freq_tree, kd_tree
+
+
+def flat_workload(n: int, side: int, L: int, tol: float, name: str = "flat", seed: int = mi.SEED_GEOMETRY):
+    """A flat-square workload with n random points and side^2 modes."""
+    return mi.Workload(name, "flat", n, side * side, "complex128", tol, L, (1,), {"side": side, "seed": seed})
+
+
+def sphere_workload(n: int, lmax: int, L: int, tol: float, name: str = "sphere"):
+    return mi.Workload(name, "sphere", n, (lmax + 1) ** 2, "float64", tol, L, (1,), {"lmax": lmax})
+
+
+def setup(w: mi.Workload):
+    """Return (basis, perm, sp_off, fr_off)."""
+    if w.family == "flat":
+        x = mi.flat_points(w.n, seed=w.extra.get("seed", mi.SEED_GEOMETRY))
+        k = mi.flat_modes(w.extra["side"])[: w.m]
+        basis = FlatBasis(x, k)
+        perm, sp_off = kd_tree(x, w.L, alternate=True)
+    elif w.family == "sphere":
+        th, ph, p = mi.sphere_points(w.n)
+        basis = SphereBasis(th, ph, w.extra["lmax"])
+        perm, sp_off = kd_tree(p, w.L, alternate=False)
+    elif w.family == "mesh":
+        from . import mesh_setup
+
+        basis, perm, sp_off = mesh_setup.setup_mesh(w)
+    else:
+        raise ValueError(w.family)
+    fr_off = freq_tree(w.m, w.L)
+    return basis, perm, sp_off, fr_off
+
+
+def build_workload_plan(w: mi.Workload, path: str, workers=None, log=print, precompute_sphere=None):
+    basis, perm, sp_off, fr_off = setup(w)
+    if isinstance(basis, SphereBasis) and (precompute_sphere or (precompute_sphere is None and w.n * w.m <= 6e9)):
+        basis.precompute_all()
+    return build_plan(basis, perm, sp_off, fr_off, w.L, w.tol, path, workers=workers, log=log)
+
+
+def plan_cache_path(w: mi.Workload, root: str | None = None) -> str:
+    root = root or os.environ.get("MHT_PLAN_DIR") or ("/dev/shm/mht_plans" if os.path.isdir("/dev/shm") else "/tmp/mht_plans")
+    os.makedirs(root, exist_ok=True)
+    tag = f"{w.name}_{w.family}_n{w.n}_m{w.m}_L{w.L}_tol{w.tol:g}"
+    ex = "_".join(f"{k}{v}" for k, v in sorted(w.extra.items()))
+    return os.path.join(root, f"{tag}_{ex}.plan")
+
+
+def ensure_plan(w: mi.Workload, workers=None, log=print, root=None) -> str:
+    """Build the plan unless a complete file for this workload already exists
+    (a cache only; a fresh box always rebuilds)."""
+    p = plan_cache_path(w, root)
+    if not os.path.exists(p):
+        build_workload_plan(w, p, workers=workers, log=log)
+    return p
+
+
+__all__ = ["flat_workload", "sphere_workload", "setup", "build_workload_plan", "ensure_plan",
+           "plan_cache_path", "DenseBasis", "dataclasses", "np"]
