@@ -1,0 +1,137 @@
+/*
+ * libmht — B200 (sm_100a) butterfly manifold-harmonic-transform apply.
+ *
+ * The C ABI of the hot path of arxiv/paper_2605_21828 ("butterfly-accelerated
+ * manifold harmonic transform", BF-MHT).  The library applies a precomputed
+ * row-wise butterfly factorization of the MHT matrix
+ *
+ *     Phi in C^{n x m},  Phi_jk = phi_k(x_j)     (§1 Eq. MHT-sum)
+ *
+ * to coefficient vectors (synthesis f = Phi c) and applies its adjoint
+ * (analysis c = Phi^* f; "fast adjoint transform", §1).  The
+ * factorization {V_nu, R_{tau nu}, U_tau} is the one of §2:
+ * leaf projection, L transfer levels, leaf interpolation, applied "one
+ * multiply per stored factor" (§6.2).  Multi-RHS
+ * (§7.1; §7.2) applies the same operator to nrhs
+ * columns.  Factor construction is a host precompute that writes a plan file
+ * (format: DESIGN.md §4); this library only loads and applies it.
+ *
+ * Conventions for every entry point
+ *  - Element type is fixed by the plan: MHT_DTYPE_C128 = interleaved complex
+ *    double (re, im) (flat square), MHT_DTYPE_F64 = double (sphere, meshes).
+ *  - Vectors are column-major blocks: c is m x nrhs with leading dimension m
+ *    (a contiguous (nrhs, m) array), f is n x nrhs with leading dimension n.
+ *  - c is in the plan's frequency order (eigenvalue order); f is in the user's
+ *    point order (the plan's perm_x maps tree order back to it).
+ *  - Device-pointer calls (mht_apply, mht_apply_adjoint) enqueue on the plan's
+ *    stream and return without synchronising; a device fault surfaces as
+ *    MHT_ERR_CUDA on a later call or on mht_sync.
+ *  - A plan owns all device memory for factors and workspace; the caller owns
+ *    c and f.  Destinations are fully overwritten (c = 0 gives f = 0 exactly).
+ *  - A plan is NOT safe for concurrent applies (shared workspace).  Different
+ *    plans may be used from different threads.
+ *  - No C++ exception crosses this boundary.  Every function returns a status;
+ *    mht_last_error() gives a thread-local detail string for the last failure.
+ */
+#ifndef MHT_H_
+#define MHT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mht_plan mht_plan; /* opaque */
+
+typedef enum {
+  MHT_OK = 0,
+  MHT_ERR_INVALID_ARG = 1, /* null pointer, nrhs < 1, bad device id        */
+  MHT_ERR_FORMAT = 2,      /* bad magic/version/checksum, chain invariant  */
+  MHT_ERR_SHAPE = 3,       /* inconsistent sizes inside the plan           */
+  MHT_ERR_OOM = 4,         /* host or device allocation failed             */
+  MHT_ERR_CUDA = 5,        /* CUDA runtime error (incl. earlier async faults) */
+  MHT_ERR_UNSUPPORTED = 6, /* no sm_100 device / feature not built          */
+  MHT_ERR_IO = 7           /* file open/read failure                        */
+} mht_status;
+
+enum { MHT_DTYPE_F64 = 1, MHT_DTYPE_C128 = 2 };
+
+typedef struct {
+  int64_t n, m;          /* rows (points) and columns (eigenfunctions) of Phi */
+  int32_t L;             /* tree depth: 2^L leaves on both trees             */
+  int32_t dtype;         /* MHT_DTYPE_F64 | MHT_DTYPE_C128                   */
+  double tol;            /* ID tolerance the plan was built with             */
+  int64_t plan_bytes;    /* bytes of the plan file                           */
+  int64_t factor_entries;/* stored non-identity coefficients (T and U)       */
+  int64_t device_bytes;  /* device memory held by factors + index tables     */
+  int64_t index_entries; /* int32 skeleton/redundant indices on the device   */
+  int32_t n_materialized;/* blocks that run (ID, DENSE, COPY)                */
+  int32_t n_alias;       /* identity blocks resolved to an alias (no work)   */
+  int32_t fwd_launches;  /* kernel launches per forward apply                */
+  int32_t adj_launches;  /* kernel launches per adjoint apply                */
+} mht_plan_info;
+
+/* Parse + validate a plan file, pack it into the level-contiguous device
+ * layout and upload it to `device` (a CUDA ordinal).  Reads the whole file
+ * once; the checksum is verified on the fly.  *out is set only on MHT_OK.
+ * Errors: MHT_ERR_IO (open/read), MHT_ERR_FORMAT (magic, version, checksum,
+ * chain invariant r_in = r_out(p,c1) + r_out(p,c2)),
+ * MHT_ERR_SHAPE, MHT_ERR_OOM, MHT_ERR_CUDA, MHT_ERR_UNSUPPORTED. */
+mht_status mht_plan_load(const char *path, int device, mht_plan **out);
+
+mht_status mht_plan_info_get(const mht_plan *plan, mht_plan_info *info);
+
+/* Stream for subsequent calls (a cudaStream_t passed as void*; NULL = the
+ * legacy default stream).  Callers using PyTorch pass
+ * torch.cuda.current_stream().cuda_stream. */
+mht_status mht_plan_set_stream(mht_plan *plan, void *stream);
+
+/* Pre-size the workspace for up to `nrhs` right-hand sides (otherwise grown
+ * on demand by the first apply with a larger nrhs, which synchronises). */
+mht_status mht_reserve(mht_plan *plan, int nrhs);
+
+/* f = Phi_BF c.  c: device, m x nrhs (ld m); f: device, n x nrhs (ld n).
+ * Runs leaf projection, the L transfer stages and the leaf interpolation
+ * (with the perm_x scatter fused into the store). */
+mht_status mht_apply(mht_plan *plan, const void *c, void *f, int nrhs);
+
+/* c = Phi_BF^* f.  f: device n x nrhs; c: device m x nrhs.  Exact reverse of
+ * mht_apply with conjugate transposes; group sums are formed on load from
+ * per-block partials (no atomics, bitwise deterministic). */
+mht_status mht_apply_adjoint(mht_plan *plan, const void *f, void *c, int nrhs);
+
+/* Same as above from/to HOST memory: copies c (or f) host->device on the plan
+ * stream, applies, copies the result device->host and synchronises.  Host
+ * buffers should be pinned for full copy bandwidth.  Used for the end-to-end
+ * measurement. */
+mht_status mht_apply_host(mht_plan *plan, const void *c_host, void *f_host, int nrhs);
+mht_status mht_apply_adjoint_host(mht_plan *plan, const void *f_host, void *c_host, int nrhs);
+
+/* Capture each (direction, nrhs, c, f) apply sequence in a CUDA graph and
+ * replay it on later calls with the same arguments (on = 1, default on). */
+mht_status mht_set_graphs(mht_plan *plan, int on);
+
+/* Block until the plan's stream is idle; returns MHT_ERR_CUDA on a fault. */
+mht_status mht_sync(mht_plan *plan);
+
+/* Per-stage statistics of the packed plan.  stage in [0, L+1].
+ *   coef_bytes: factor bytes read by the stage per apply (per RHS column);
+ *   n_tiles_fwd / n_tiles_adj: work tiles; n_mat: materialised blocks. */
+mht_status mht_stage_stats(const mht_plan *plan, int stage, int64_t *coef_bytes,
+                           int32_t *n_mat, int32_t *n_tiles_fwd, int32_t *n_tiles_adj);
+
+/* Destroy the plan (synchronises its stream first).  NULL is a no-op. */
+void mht_plan_destroy(mht_plan *plan);
+
+const char *mht_status_string(mht_status s);
+const char *mht_last_error(void);
+
+/* Library build identification ("sm_100a ..."). */
+const char *mht_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MHT_H_ */

@@ -1,0 +1,84 @@
+// Internal device-side layout of a loaded butterfly plan (libmht).
+//
+// The plan file's per-stage block tables are resolved on the
+// host into a flat list of *materialised* blocks — the ones that do work —
+// plus per-stage tile lists.  IDENTITY blocks whose two input segments are
+// adjacent in memory become aliases and cost nothing (SURVEY.md §8(a) a2:
+// "the level permutation lives in these offsets").
+#pragma once
+#include <cstdint>
+
+namespace mht {
+
+enum : int32_t {
+  SRC_C = 0,     // user coefficient vector c (ld = m)
+  SRC_Z = 1,     // plan workspace zpool (ld = Zt)
+};
+
+enum : int32_t {
+  F_SKEL_IOTA = 1,  // skeleton positions are 0..n_skel-1 (COPY blocks)
+  F_RED_IOTA = 2,   // redundant positions are 0..n_red-1 (DENSE blocks)
+  F_OUT_F = 4,      // output rows go to f through perm_x (leaf stage)
+};
+
+// One materialised block: out[i] = in[skel[i]] (i < n_skel) + sum_j T[i,j] in[red[j]]
+// with in = concat(seg0, seg1), T column-major r_out x n_red (ld = r_out).
+struct DevBlock {
+  int64_t coef_off;    // element offset of T in the coefficient pool
+  int64_t skel_off;    // offset into the index pool (ID blocks)
+  int64_t red_off;     // offset into the index pool (ID blocks)
+  int64_t seg_off[2];  // element offset of each input segment in its source
+  int64_t out_off;     // zpool offset (stages 0..L) or sp_off row (leaf stage)
+  int64_t part_off;    // adjoint partial slot (r_in entries)
+  int32_t seg_len[2];
+  int32_t seg_src[2];  // SRC_C | SRC_Z
+  int32_t r_out, r_in, n_skel, n_red;
+  int32_t flags, pad;
+};
+static_assert(sizeof(DevBlock) == 96, "DevBlock layout");
+
+// A unit of work: rows [start, start+count) (forward) or redundant columns
+// [start, start+count) (adjoint) of block `blk`.
+struct Tile {
+  int32_t blk, start, count, pad;
+};
+
+// Adjoint group-sum piece: dst[dst_off + i] = sum_r part[rd[rd_begin + r] + i].
+struct Piece {
+  int64_t dst_off;
+  int64_t rd_begin;
+  int32_t dst_src;  // SRC_C | SRC_Z
+  int32_t len;
+  int32_t rd_count;
+  int32_t pad;
+};
+
+struct Ctx {  // per-launch pointers
+  const void *coef;
+  const int32_t *idx;
+  const int32_t *perm;
+  const DevBlock *blocks;
+  const void *c;   // SRC_C base
+  void *cw;        // writable c (adjoint output)
+  void *z;         // zpool
+  void *part;      // partial pool
+  const void *fin; // f input (adjoint)
+  void *fout;      // f output (forward)
+  int64_t m, n, Zt, Pt;
+  int nrhs;
+};
+
+constexpr int FWD_ROWS = 64;     // rows per forward tile (2 per lane)
+constexpr int FWD_THREADS = 128; // 4 warps split the columns
+constexpr int ADJ_COLS = 32;     // redundant columns per adjoint tile (8 per warp)
+constexpr int ADJ_THREADS = 128;
+constexpr int ADJ_RCH = 256;     // adjoint rows staged in smem per pass
+
+// Launchers (mht_kernels.cu).  is_complex selects double2 vs double.
+void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, void *stream);
+void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
+                void *stream);
+void launch_reduce(bool is_complex, const Ctx &ctx, const Piece *pieces, const int64_t *rd,
+                   int npieces, void *stream);
+
+}  // namespace mht

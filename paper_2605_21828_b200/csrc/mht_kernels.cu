@@ -1,0 +1,327 @@
+// libmht device kernels (sm_100a): butterfly apply / adjoint stages.
+//
+// PAPER.md §2: every stage multiplies each stored factor once —
+//   forward   out = in[skel] + T in[red]          (ID transfer, X = [I T] Pi)
+//   adjoint   w[skel] = z,  w[red] = T^* z        (X^*; conjugate for complex)
+// with in = [z(p,c1); z(p,c2)] gathered from two segments (level permutation
+// fused into the load addressing) and the leaf stage's perm_x scatter fused
+// into the store.  fp64 real (double) or complex (double2).
+//
+// nrhs = 1 is HBM-bound (0.5 flop/B complex): T is streamed once with 16-byte
+// non-allocating loads, each warp reading 32 consecutive rows (512 B) of a
+// column.  Multi-RHS reuses each T element for RB right-hand sides held in
+// registers.
+#include <cuda_runtime.h>
+
+#include "mht_internal.cuh"
+
+namespace mht {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <class S>
+struct Tr;
+
+template <>
+struct Tr<double> {
+  static __device__ __forceinline__ double zero() { return 0.0; }
+  static __device__ __forceinline__ void fma(double &a, double t, double x) { a = ::fma(t, x, a); }
+  static __device__ __forceinline__ void fmac(double &a, double t, double z) { a = ::fma(t, z, a); }
+  static __device__ __forceinline__ double add(double a, double b) { return a + b; }
+  static __device__ __forceinline__ double shfl(double v, int s) { return __shfl_sync(FULL, v, s); }
+  static __device__ __forceinline__ double shfl_xor(double v, int s) {
+    return __shfl_xor_sync(FULL, v, s);
+  }
+  static __device__ __forceinline__ double ldT(const double *p) {
+    double v;
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+  }
+};
+
+template <>
+struct Tr<double2> {
+  static __device__ __forceinline__ double2 zero() { return make_double2(0.0, 0.0); }
+  // a += t * x
+  static __device__ __forceinline__ void fma(double2 &a, double2 t, double2 x) {
+    a.x = ::fma(t.x, x.x, a.x);
+    a.x = ::fma(-t.y, x.y, a.x);
+    a.y = ::fma(t.x, x.y, a.y);
+    a.y = ::fma(t.y, x.x, a.y);
+  }
+  // a += conj(t) * z
+  static __device__ __forceinline__ void fmac(double2 &a, double2 t, double2 z) {
+    a.x = ::fma(t.x, z.x, a.x);
+    a.x = ::fma(t.y, z.y, a.x);
+    a.y = ::fma(t.x, z.y, a.y);
+    a.y = ::fma(-t.y, z.x, a.y);
+  }
+  static __device__ __forceinline__ double2 add(double2 a, double2 b) {
+    return make_double2(a.x + b.x, a.y + b.y);
+  }
+  static __device__ __forceinline__ double2 shfl(double2 v, int s) {
+    return make_double2(__shfl_sync(FULL, v.x, s), __shfl_sync(FULL, v.y, s));
+  }
+  static __device__ __forceinline__ double2 shfl_xor(double2 v, int s) {
+    return make_double2(__shfl_xor_sync(FULL, v.x, s), __shfl_xor_sync(FULL, v.y, s));
+  }
+  static __device__ __forceinline__ double2 ldT(const double2 *p) {
+    double2 v;
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+  }
+};
+
+// in[q] for right-hand side r: two segments, each in c (ld m) or zpool (ld Zt).
+template <class S>
+__device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, int r) {
+  const bool s1 = q >= B.seg_len[0];  // no dynamic indexing: keeps B in registers
+  const int64_t off = s1 ? B.seg_off[1] + (q - B.seg_len[0]) : B.seg_off[0] + q;
+  const int32_t src = s1 ? B.seg_src[1] : B.seg_src[0];
+  if (src == SRC_C) return static_cast<const S *>(cx.c)[r * cx.m + off];
+  return static_cast<const S *>(cx.z)[r * cx.Zt + off];
+}
+
+// ------------------------------------------------------------------------
+// forward stage: one CTA per (block, 64-row tile); 4 warps split the
+// redundant columns, lane l owns rows l and l+32 of the tile.
+// ------------------------------------------------------------------------
+template <class S, int RB>
+__global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Tile *__restrict__ tiles) {
+  using X = Tr<S>;
+  const Tile tl = tiles[blockIdx.x];
+  const DevBlock B = cx.blocks[tl.blk];
+  const int rhs0 = blockIdx.y * RB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ra = tl.start + lane, rb = tl.start + 32 + lane;
+  const bool va = lane < tl.count, vb = lane + 32 < tl.count;
+  S acc_a[RB], acc_b[RB];
+#pragma unroll
+  for (int k = 0; k < RB; ++k) acc_a[k] = acc_b[k] = X::zero();
+
+  const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
+  const int64_t ld = B.r_out;
+  for (int j0 = warp * 32; j0 < B.n_red; j0 += FWD_THREADS) {
+    const int j = j0 + lane;
+    S xr[RB];
+#pragma unroll
+    for (int k = 0; k < RB; ++k) xr[k] = X::zero();
+    if (j < B.n_red) {
+      const int q = (B.flags & F_RED_IOTA) ? j : cx.idx[B.red_off + j];
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        if (rhs0 + k < cx.nrhs) xr[k] = in_value<S>(cx, B, q, rhs0 + k);
+    }
+    const int jn = min(32, B.n_red - j0);
+    const S *col = T + (int64_t)j0 * ld;
+    if (jn == 32) {
+#pragma unroll 8
+      for (int jj = 0; jj < 32; ++jj) {
+        const S ta = va ? X::ldT(col + (int64_t)jj * ld + ra) : X::zero();
+        const S tb = vb ? X::ldT(col + (int64_t)jj * ld + rb) : X::zero();
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+          const S x = X::shfl(xr[k], jj);
+          X::fma(acc_a[k], ta, x);
+          X::fma(acc_b[k], tb, x);
+        }
+      }
+    } else {
+      for (int jj = 0; jj < jn; ++jj) {
+        const S ta = va ? X::ldT(col + (int64_t)jj * ld + ra) : X::zero();
+        const S tb = vb ? X::ldT(col + (int64_t)jj * ld + rb) : X::zero();
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+          const S x = X::shfl(xr[k], jj);
+          X::fma(acc_a[k], ta, x);
+          X::fma(acc_b[k], tb, x);
+        }
+      }
+    }
+  }
+  __shared__ S red[FWD_THREADS / 32][FWD_ROWS][RB];
+#pragma unroll
+  for (int k = 0; k < RB; ++k) {
+    red[warp][lane][k] = acc_a[k];
+    red[warp][lane + 32][k] = acc_b[k];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < FWD_ROWS * RB; e += FWD_THREADS) {
+    const int i = e % FWD_ROWS, k = e / FWD_ROWS;
+    const int r = rhs0 + k;
+    if (i >= tl.count || r >= cx.nrhs) continue;
+    S s = red[0][i][k];
+#pragma unroll
+    for (int w = 1; w < FWD_THREADS / 32; ++w) s = X::add(s, red[w][i][k]);
+    const int row = tl.start + i;
+    if (row < B.n_skel) {
+      const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
+      s = X::add(s, in_value<S>(cx, B, q, r));
+    }
+    if (B.flags & F_OUT_F) {
+      const int64_t j = cx.perm[B.out_off + row];
+      static_cast<S *>(cx.fout)[r * cx.n + j] = s;
+    } else {
+      static_cast<S *>(cx.z)[r * cx.Zt + B.out_off + row] = s;
+    }
+  }
+}
+
+// adjoint input z[i] of a block (its zpool slot, or f through perm_x for the leaf stage)
+template <class S>
+__device__ __forceinline__ S adj_in(const Ctx &cx, const DevBlock &B, int i, int r, bool from_f) {
+  if (from_f) return static_cast<const S *>(cx.fin)[r * cx.n + cx.perm[B.out_off + i]];
+  return static_cast<const S *>(cx.z)[r * cx.Zt + B.out_off + i];
+}
+
+// ------------------------------------------------------------------------
+// adjoint stage: one CTA per (block, 32 redundant columns); warp w owns 8
+// columns and computes their conj-dot products with z over all r_out rows
+// (rows staged through shared memory, ADJ_RCH at a time).
+// ------------------------------------------------------------------------
+template <class S, int RB>
+__global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Tile *__restrict__ tiles,
+                                                         int from_f) {
+  using X = Tr<S>;
+  constexpr int CPW = ADJ_COLS / (ADJ_THREADS / 32);  // columns per warp = 8
+  const Tile tl = tiles[blockIdx.x];
+  const DevBlock B = cx.blocks[tl.blk];
+  const int rhs0 = blockIdx.y * RB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ S zs[ADJ_RCH][RB];
+  S acc[CPW][RB];
+#pragma unroll
+  for (int u = 0; u < CPW; ++u)
+#pragma unroll
+    for (int k = 0; k < RB; ++k) acc[u][k] = X::zero();
+  const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
+  const int64_t ld = B.r_out;
+  const int cbase = tl.start + warp * CPW;
+  const int cend = tl.start + tl.count;
+
+  for (int rc = 0; rc < B.r_out; rc += ADJ_RCH) {
+    const int rn = min(ADJ_RCH, B.r_out - rc);
+    for (int e = threadIdx.x; e < rn * RB; e += ADJ_THREADS) {
+      const int i = e % rn, k = e / rn;
+      zs[i][k] = (rhs0 + k < cx.nrhs) ? adj_in<S>(cx, B, rc + i, rhs0 + k, from_f) : X::zero();
+    }
+    __syncthreads();
+    if (cbase < cend) {
+      for (int i = lane; i < rn; i += 32) {
+        S zv[RB];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) zv[k] = zs[i][k];
+#pragma unroll
+        for (int u = 0; u < CPW; ++u) {
+          if (cbase + u < cend) {
+            const S t = X::ldT(T + (int64_t)(cbase + u) * ld + rc + i);
+#pragma unroll
+            for (int k = 0; k < RB; ++k) X::fmac(acc[u][k], t, zv[k]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // warp reductions
+#pragma unroll
+  for (int u = 0; u < CPW; ++u)
+#pragma unroll
+    for (int k = 0; k < RB; ++k)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[u][k] = X::add(acc[u][k], X::shfl_xor(acc[u][k], o));
+  if (lane == 0) {
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+      const int col = cbase + u;
+      if (col >= cend) continue;
+      const int q = (B.flags & F_RED_IOTA) ? col : cx.idx[B.red_off + col];
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        if (rhs0 + k < cx.nrhs) static_cast<S *>(cx.part)[(rhs0 + k) * cx.Pt + B.part_off + q] = acc[u][k];
+    }
+  }
+  // skeleton part: w[skel[i]] = z[i]  (written once, by the block's first tile)
+  if (tl.start == 0 && B.n_skel > 0) {
+    for (int e = threadIdx.x; e < B.n_skel * RB; e += ADJ_THREADS) {
+      const int i = e % B.n_skel, k = e / B.n_skel;
+      if (rhs0 + k >= cx.nrhs) continue;
+      const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
+      static_cast<S *>(cx.part)[(rhs0 + k) * cx.Pt + B.part_off + q] = adj_in<S>(cx, B, i, rhs0 + k, from_f);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------
+// adjoint group sums: dst = sum of the readers' partial ranges (fixed order,
+// no atomics).
+// ------------------------------------------------------------------------
+template <class S>
+__global__ void __launch_bounds__(256) reduce_kernel(const Ctx cx, const Piece *__restrict__ pieces,
+                                                     const int64_t *__restrict__ rd) {
+  using X = Tr<S>;
+  const Piece p = pieces[blockIdx.x];
+  const S *part = static_cast<const S *>(cx.part);
+  for (int r = blockIdx.y; r < cx.nrhs; r += gridDim.y) {
+    for (int i = threadIdx.x; i < p.len; i += blockDim.x) {
+      S s = X::zero();
+      for (int q = 0; q < p.rd_count; ++q) s = X::add(s, part[r * cx.Pt + rd[p.rd_begin + q] + i]);
+      if (p.dst_src == SRC_C)
+        static_cast<S *>(cx.cw)[r * cx.m + p.dst_off + i] = s;
+      else
+        static_cast<S *>(cx.z)[r * cx.Zt + p.dst_off + i] = s;
+    }
+  }
+}
+
+template <class S>
+void fwd_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, cudaStream_t st) {
+  if (cx.nrhs == 1) {
+    fwd_kernel<S, 1><<<dim3(ntiles, 1), FWD_THREADS, 0, st>>>(cx, tiles);
+  } else {
+    constexpr int RB = 4;
+    fwd_kernel<S, RB><<<dim3(ntiles, (cx.nrhs + RB - 1) / RB), FWD_THREADS, 0, st>>>(cx, tiles);
+  }
+}
+
+template <class S>
+void adj_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cudaStream_t st) {
+  if (cx.nrhs == 1) {
+    adj_kernel<S, 1><<<dim3(ntiles, 1), ADJ_THREADS, 0, st>>>(cx, tiles, from_f);
+  } else {
+    constexpr int RB = 2;
+    adj_kernel<S, RB><<<dim3(ntiles, (cx.nrhs + RB - 1) / RB), ADJ_THREADS, 0, st>>>(cx, tiles, from_f);
+  }
+}
+
+}  // namespace
+
+void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, void *stream) {
+  if (ntiles <= 0) return;
+  if (is_complex)
+    fwd_dispatch<double2>(ctx, tiles, ntiles, (cudaStream_t)stream);
+  else
+    fwd_dispatch<double>(ctx, tiles, ntiles, (cudaStream_t)stream);
+}
+
+void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
+                void *stream) {
+  if (ntiles <= 0) return;
+  if (is_complex)
+    adj_dispatch<double2>(ctx, tiles, ntiles, in_from_f ? 1 : 0, (cudaStream_t)stream);
+  else
+    adj_dispatch<double>(ctx, tiles, ntiles, in_from_f ? 1 : 0, (cudaStream_t)stream);
+}
+
+void launch_reduce(bool is_complex, const Ctx &ctx, const Piece *pieces, const int64_t *rd,
+                   int npieces, void *stream) {
+  if (npieces <= 0) return;
+  const int gy = ctx.nrhs < 8 ? ctx.nrhs : 8;
+  if (is_complex)
+    reduce_kernel<double2><<<dim3(npieces, gy), 256, 0, (cudaStream_t)stream>>>(ctx, pieces, rd);
+  else
+    reduce_kernel<double><<<dim3(npieces, gy), 256, 0, (cudaStream_t)stream>>>(ctx, pieces, rd);
+}
+
+}  // namespace mht

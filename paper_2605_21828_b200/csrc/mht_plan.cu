@@ -1,0 +1,770 @@
+// libmht host runtime: plan loader, device layout, apply sequencing, C ABI.
+//
+// Loader (DESIGN.md §4 / §5):
+//  1. stream the plan file once through two pinned 64 MiB buffers: factor
+//     coefficients go straight to the device pool, the block tables and
+//     index pools stay on the host; the u64 checksum is summed on the fly;
+//  2. validate the chain invariant r_in(l,(t,v)) = r_out(l-1,(p,2v)) +
+//     r_out(l-1,(p,2v+1)) and the leaf sizes;
+//  3. resolve every block's input to <= 2 contiguous segments.  IDENTITY
+//     blocks whose inputs are adjacent become aliases (no work, no bytes);
+//     the others become COPY blocks.  This is where the level permutation is
+//     fused into load addressing (north_star subsystem (2));
+//  4. build size-sorted (LPT) forward row tiles and adjoint column tiles per
+//     stage, and the adjoint group-sum pieces (sum-of-partials, no atomics);
+//  5. upload the tables.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/mht.h"
+#include "mht_internal.cuh"
+
+using namespace mht;
+
+namespace {
+thread_local std::string g_err;
+
+mht_status fail(mht_status s, const std::string &msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(x)                                                                       \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? MHT_ERR_OOM : MHT_ERR_CUDA,           \
+                  std::string(#x) + ": " + cudaGetErrorString(e_));                       \
+  } while (0)
+
+struct FileBlock {
+  int32_t kind, r_out, r_in, pad;
+  int64_t idx_off, coef_off;
+};
+static_assert(sizeof(FileBlock) == 32, "block record");
+
+struct Range {
+  int32_t off = 0, count = 0;
+};
+
+}  // namespace
+
+struct mht_plan {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool cplx = false;
+  size_t ssz = 8;
+  int64_t n = 0, m = 0;
+  int L = 0;
+  double tol = 0;
+  int64_t plan_bytes = 0, factor_entries = 0, index_entries = 0, device_bytes = 0;
+  int n_mat = 0, n_alias = 0;
+  bool graphs = true;
+
+  void *d_coef = nullptr;
+  int32_t *d_idx = nullptr;
+  int32_t *d_perm = nullptr;
+  DevBlock *d_blocks = nullptr;
+  Tile *d_fwd = nullptr;
+  Tile *d_adj = nullptr;
+  Piece *d_pieces = nullptr;
+  int64_t *d_rd = nullptr;
+
+  std::vector<Range> fwd, adj, pieces;  // per stage 0..L+1
+  Range cpieces;
+  std::vector<int64_t> stage_coef_bytes;
+  std::vector<int32_t> stage_nmat;
+  int64_t Zt = 0, Pt = 0;
+
+  void *d_z = nullptr, *d_part = nullptr;
+  int ws_nrhs = 0;
+  void *d_hc = nullptr, *d_hf = nullptr;
+  int host_nrhs = 0;
+
+  ~mht_plan() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd,
+                    (void *)d_adj, (void *)d_pieces, (void *)d_rd, d_z, d_part, d_hc, d_hf})
+      if (p) cudaFree(p);
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- file IO
+struct Reader {
+  FILE *fp = nullptr;
+  uint64_t csum = 0;
+  int64_t body_read = 0;
+  ~Reader() {
+    if (fp) fclose(fp);
+  }
+  bool read(void *dst, size_t bytes, bool in_body = true) {
+    if (bytes == 0) return true;
+    if (fread(dst, 1, bytes, fp) != bytes) return false;
+    if (in_body) {
+      const uint64_t *w = static_cast<const uint64_t *>(dst);
+      uint64_t s = 0;
+      for (size_t i = 0; i < bytes / 8; ++i) s += w[i];
+      csum += s;
+      body_read += (int64_t)bytes;
+    }
+    return true;
+  }
+};
+
+size_t pad8(size_t b) { return (b + 7) / 8 * 8; }
+
+template <class T>
+mht_status upload(T **dptr, const std::vector<T> &v, int64_t &acct) {
+  size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
+  CUDA_TRY(cudaMalloc((void **)dptr, bytes));
+  acct += (int64_t)bytes;
+  if (!v.empty()) CUDA_TRY(cudaMemcpy(*dptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return MHT_OK;
+}
+
+struct Loc {
+  int32_t src = SRC_C;
+  int64_t off = 0;
+};
+
+mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P) {
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(MHT_ERR_INVALID_ARG, "bad device ordinal");
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(MHT_ERR_UNSUPPORTED, "libmht is built for sm_100a (B200)");
+  CUDA_TRY(cudaSetDevice(device));
+  P->device = device;
+
+  Reader R;
+  R.fp = fopen(path, "rb");
+  if (!R.fp) return fail(MHT_ERR_IO, std::string("cannot open ") + path);
+  fseeko(R.fp, 0, SEEK_END);
+  const int64_t fbytes = ftello(R.fp);
+  fseeko(R.fp, 0, SEEK_SET);
+  unsigned char hdr[256];
+  if (fbytes < 256 || !R.read(hdr, 256, false)) return fail(MHT_ERR_FORMAT, "short header");
+  if (memcmp(hdr, "BFMHTPLN", 8) != 0) return fail(MHT_ERR_FORMAT, "bad magic");
+  uint32_t ver, dt;
+  int64_t nst, body;
+  uint64_t csum;
+  int32_t L;
+  memcpy(&ver, hdr + 8, 4);
+  memcpy(&dt, hdr + 12, 4);
+  memcpy(&P->n, hdr + 16, 8);
+  memcpy(&P->m, hdr + 24, 8);
+  memcpy(&L, hdr + 32, 4);
+  memcpy(&P->tol, hdr + 40, 8);
+  memcpy(&nst, hdr + 48, 8);
+  memcpy(&csum, hdr + 56, 8);
+  memcpy(&body, hdr + 64, 8);
+  if (ver != 1) return fail(MHT_ERR_FORMAT, "unsupported plan version");
+  if (dt != 1 && dt != 2) return fail(MHT_ERR_FORMAT, "bad dtype");
+  if (L < 0 || L > 24 || nst != L + 2) return fail(MHT_ERR_FORMAT, "bad L / stage count");
+  if (body < 0 || body + 256 != fbytes) return fail(MHT_ERR_FORMAT, "body size mismatch");
+  if (P->n < 1 || P->m < 1 || P->n > INT32_MAX || P->m > INT32_MAX) return fail(MHT_ERR_SHAPE, "bad n/m");
+  P->L = L;
+  P->cplx = dt == 2;
+  P->ssz = P->cplx ? 16 : 8;
+  P->plan_bytes = fbytes;
+  const int64_t nl = int64_t(1) << L;
+
+  std::vector<int32_t> perm((size_t)pad8(4 * P->n) / 4);
+  std::vector<int64_t> sp_off(nl + 1), fr_off(nl + 1);
+  if (!R.read(perm.data(), pad8(4 * P->n)) || !R.read(sp_off.data(), 8 * (nl + 1)) ||
+      !R.read(fr_off.data(), 8 * (nl + 1)))
+    return fail(MHT_ERR_FORMAT, "truncated trees");
+  perm.resize(P->n);
+  if (sp_off[0] != 0 || sp_off[nl] != P->n || fr_off[0] != 0 || fr_off[nl] != P->m)
+    return fail(MHT_ERR_FORMAT, "tree offsets do not cover n / m");
+  for (int64_t i = 0; i < nl; ++i)
+    if (sp_off[i + 1] < sp_off[i] || fr_off[i + 1] < fr_off[i])
+      return fail(MHT_ERR_FORMAT, "tree offsets not monotone");
+  {
+    std::vector<char> seen(P->n, 0);
+    for (int32_t j : perm) {
+      if (j < 0 || j >= P->n || seen[j]) return fail(MHT_ERR_FORMAT, "perm_x is not a permutation");
+      seen[j] = 1;
+    }
+  }
+
+  // device coefficient pool: the body size bounds the coefficient bytes
+  CUDA_TRY(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  const size_t pool_bytes = std::max<int64_t>(16, body);
+  CUDA_TRY(cudaMalloc(&P->d_coef, pool_bytes));
+  P->device_bytes += (int64_t)pool_bytes;
+
+  const size_t CH = size_t(64) << 20;
+  void *pin[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2];
+  CUDA_TRY(cudaHostAlloc(&pin[0], CH, cudaHostAllocDefault));
+  CUDA_TRY(cudaHostAlloc(&pin[1], CH, cudaHostAllocDefault));
+  CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  struct PinGuard {
+    void **p;
+    cudaEvent_t *e;
+    ~PinGuard() {
+      cudaFreeHost(p[0]);
+      cudaFreeHost(p[1]);
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
+    }
+  } pg{pin, ev};
+  int which = 0;
+  bool pending[2] = {false, false};
+
+  std::vector<std::vector<FileBlock>> blk(L + 2);
+  std::vector<std::vector<int32_t>> idx(L + 2);
+  std::vector<int64_t> coef_base(L + 2), ncoef_s(L + 2);
+  int64_t coef_cursor = 0;  // in scalars
+  for (int s = 0; s < L + 2; ++s) {
+    int64_t sh[4];
+    if (!R.read(sh, 32)) return fail(MHT_ERR_FORMAT, "truncated stage header");
+    if (sh[0] != s || sh[1] != nl || sh[2] < 0 || sh[3] < 0) return fail(MHT_ERR_FORMAT, "bad stage header");
+    const int64_t nidx = sh[2], ncoef = sh[3];
+    if ((coef_cursor + ncoef) * (int64_t)P->ssz > (int64_t)pool_bytes) return fail(MHT_ERR_FORMAT, "coefficients overflow body");
+    coef_base[s] = coef_cursor;
+    ncoef_s[s] = ncoef;
+    int64_t left = ncoef * (int64_t)P->ssz;
+    char *dst = static_cast<char *>(P->d_coef) + coef_cursor * (int64_t)P->ssz;
+    while (left > 0) {
+      size_t b = (size_t)std::min<int64_t>(left, (int64_t)CH);
+      if (pending[which]) CUDA_TRY(cudaEventSynchronize(ev[which]));
+      if (!R.read(pin[which], b)) return fail(MHT_ERR_FORMAT, "truncated coefficients");
+      CUDA_TRY(cudaMemcpyAsync(dst, pin[which], b, cudaMemcpyHostToDevice, P->stream));
+      CUDA_TRY(cudaEventRecord(ev[which], P->stream));
+      pending[which] = true;
+      which ^= 1;
+      dst += b;
+      left -= (int64_t)b;
+    }
+    coef_cursor += ncoef;
+    blk[s].resize(nl);
+    if (!R.read(blk[s].data(), 32 * nl)) return fail(MHT_ERR_FORMAT, "truncated block table");
+    idx[s].resize(pad8(4 * nidx) / 4);
+    if (!R.read(idx[s].data(), pad8(4 * nidx))) return fail(MHT_ERR_FORMAT, "truncated index pool");
+    idx[s].resize(nidx);
+  }
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  if (R.body_read != body) return fail(MHT_ERR_FORMAT, "trailing bytes after last stage");
+  if (R.csum != csum) return fail(MHT_ERR_FORMAT, "checksum mismatch");
+  P->factor_entries = coef_cursor;
+
+  // ------------------------------------------------ validation
+  auto bad_block = [&](int s, int64_t b, const char *why) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "stage %d block %lld: %s", s, (long long)b, why);
+    return fail(MHT_ERR_FORMAT, buf);
+  };
+  for (int s = 0; s < L + 2; ++s) {
+    for (int64_t b = 0; b < nl; ++b) {
+      const FileBlock &B = blk[s][b];
+      if (B.r_out < 0 || B.r_in < 0) return bad_block(s, b, "negative size");
+      int64_t want_in;
+      if (s == 0) {
+        want_in = fr_off[b + 1] - fr_off[b];
+      } else if (s <= L) {
+        const int64_t nf = nl >> s, nfp = nl >> (s - 1), t = b / nf, v = b % nf, p = t >> 1;
+        want_in = (int64_t)blk[s - 1][p * nfp + 2 * v].r_out + blk[s - 1][p * nfp + 2 * v + 1].r_out;
+      } else {
+        want_in = blk[L][b].r_out;
+        if (B.r_out != sp_off[b + 1] - sp_off[b]) return bad_block(s, b, "leaf rows != |tau|");
+      }
+      if (B.r_in != want_in) return bad_block(s, b, "chain invariant r_in = r(p,c1)+r(p,c2) violated");
+      if (B.kind == 0) {
+        if (B.r_out != B.r_in) return bad_block(s, b, "IDENTITY with r_out != r_in");
+      } else if (B.kind == 1) {
+        if (B.r_out > B.r_in) return bad_block(s, b, "ID with r_out > r_in");
+        if (B.idx_off < 0 || B.idx_off + B.r_in > (int64_t)idx[s].size()) return bad_block(s, b, "index range");
+        if (B.coef_off < 0 || B.coef_off + (int64_t)B.r_out * (B.r_in - B.r_out) > ncoef_s[s])
+          return bad_block(s, b, "coefficient range");
+        for (int i = 0; i < B.r_in; ++i) {
+          int32_t q = idx[s][B.idx_off + i];
+          if (q < 0 || q >= B.r_in) return bad_block(s, b, "index out of range");
+        }
+      } else if (B.kind == 2) {
+        if (B.coef_off < 0 || B.coef_off + (int64_t)B.r_out * B.r_in > ncoef_s[s])
+          return bad_block(s, b, "coefficient range");
+      } else {
+        return bad_block(s, b, "unknown kind");
+      }
+    }
+  }
+
+  // ------------------------------------------------ resolution
+  std::vector<int32_t> idx_all;
+  std::vector<int64_t> idx_base(L + 2);
+  for (int s = 0; s < L + 2; ++s) {
+    idx_base[s] = (int64_t)idx_all.size();
+    idx_all.insert(idx_all.end(), idx[s].begin(), idx[s].end());
+  }
+  P->index_entries = (int64_t)idx_all.size();
+
+  std::vector<DevBlock> blocks;
+  std::vector<int> block_stage;
+  std::vector<std::vector<Loc>> loc(L + 1, std::vector<Loc>(nl));
+  int64_t Z = 0, Pp = 0;
+  P->stage_coef_bytes.assign(L + 2, 0);
+  P->stage_nmat.assign(L + 2, 0);
+  auto materialize = [&](int s, const FileBlock &F, Loc a, int32_t la, Loc bb, int32_t lb, bool leaf,
+                         int64_t leaf_row0) {
+    DevBlock D;
+    memset(&D, 0, sizeof D);
+    D.seg_src[0] = a.src;
+    D.seg_off[0] = a.off;
+    D.seg_len[0] = la;
+    D.seg_src[1] = bb.src;
+    D.seg_off[1] = bb.off;
+    D.seg_len[1] = lb;
+    D.r_out = F.r_out;
+    D.r_in = F.r_in;
+    if (F.kind == 1) {
+      D.n_skel = F.r_out;
+      D.n_red = F.r_in - F.r_out;
+      D.skel_off = idx_base[s] + F.idx_off;
+      D.red_off = D.skel_off + F.r_out;
+      D.coef_off = coef_base[s] + F.coef_off;
+      P->stage_coef_bytes[s] += (int64_t)F.r_out * (F.r_in - F.r_out) * (int64_t)P->ssz;
+    } else if (F.kind == 2) {
+      D.n_skel = 0;
+      D.n_red = F.r_in;
+      D.flags |= F_RED_IOTA;
+      D.coef_off = coef_base[s] + F.coef_off;
+      P->stage_coef_bytes[s] += (int64_t)F.r_out * F.r_in * (int64_t)P->ssz;
+    } else {  // COPY
+      D.n_skel = F.r_in;
+      D.n_red = 0;
+      D.flags |= F_SKEL_IOTA;
+    }
+    if (leaf) {
+      D.flags |= F_OUT_F;
+      D.out_off = leaf_row0;
+    } else {
+      D.out_off = Z;
+      Z += F.r_out;
+    }
+    D.part_off = Pp;
+    Pp += F.r_in;
+    blocks.push_back(D);
+    block_stage.push_back(s);
+    P->stage_nmat[s] += 1;
+    return Loc{SRC_Z, D.out_off};
+  };
+  for (int64_t v = 0; v < nl; ++v) {
+    const FileBlock &F = blk[0][v];
+    Loc c0{SRC_C, fr_off[v]};
+    if (F.kind == 0) {
+      loc[0][v] = c0;
+      P->n_alias++;
+    } else {
+      loc[0][v] = materialize(0, F, c0, F.r_in, Loc{SRC_C, 0}, 0, false, 0);
+    }
+  }
+  for (int s = 1; s <= L; ++s) {
+    const int64_t nf = nl >> s, nfp = nl >> (s - 1);
+    for (int64_t b = 0; b < nl; ++b) {
+      const int64_t t = b / nf, v = b % nf, p = t >> 1;
+      const int64_t b1 = p * nfp + 2 * v, b2 = b1 + 1;
+      const Loc A = loc[s - 1][b1], B = loc[s - 1][b2];
+      const int32_t la = blk[s - 1][b1].r_out, lb = blk[s - 1][b2].r_out;
+      const FileBlock &F = blk[s][b];
+      if (F.kind == 0) {
+        if (lb == 0) {
+          loc[s][b] = A;
+          P->n_alias++;
+          continue;
+        }
+        if (la == 0) {
+          loc[s][b] = B;
+          P->n_alias++;
+          continue;
+        }
+        if (A.src == B.src && A.off + la == B.off) {
+          loc[s][b] = A;
+          P->n_alias++;
+          continue;
+        }
+      }
+      loc[s][b] = materialize(s, F, A, la, B, lb, false, 0);
+    }
+  }
+  for (int64_t t = 0; t < nl; ++t) {
+    const FileBlock &F = blk[L + 1][t];
+    materialize(L + 1, F, loc[L][t], blk[L][t].r_out, Loc{SRC_C, 0}, 0, true, sp_off[t]);
+  }
+  P->Zt = std::max<int64_t>(Z, 1);
+  P->Pt = std::max<int64_t>(Pp, 1);
+  P->n_mat = (int)blocks.size();
+
+  // ------------------------------------------------ tiles (LPT order per stage)
+  std::vector<std::vector<std::pair<int64_t, Tile>>> ft(L + 2), at(L + 2);
+  for (int i = 0; i < (int)blocks.size(); ++i) {
+    const DevBlock &D = blocks[i];
+    const int s = block_stage[i];
+    for (int r0 = 0; r0 < D.r_out; r0 += FWD_ROWS) {
+      int cnt = std::min(FWD_ROWS, D.r_out - r0);
+      ft[s].push_back({(int64_t)cnt * (D.n_red + 4), Tile{i, r0, cnt, 0}});
+    }
+    if (D.n_red == 0) {
+      at[s].push_back({(int64_t)D.r_out + D.n_skel, Tile{i, 0, 0, 0}});
+    } else {
+      for (int c0 = 0; c0 < D.n_red; c0 += ADJ_COLS) {
+        int cnt = std::min(ADJ_COLS, D.n_red - c0);
+        at[s].push_back({(int64_t)cnt * (D.r_out + 4) + (c0 == 0 ? D.n_skel : 0), Tile{i, c0, cnt, 0}});
+      }
+    }
+  }
+  std::vector<Tile> fwd_all, adj_all;
+  P->fwd.assign(L + 2, Range{});
+  P->adj.assign(L + 2, Range{});
+  auto by_cost = [](const std::pair<int64_t, Tile> &a, const std::pair<int64_t, Tile> &b) {
+    return a.first > b.first;
+  };
+  for (int s = 0; s < L + 2; ++s) {
+    std::stable_sort(ft[s].begin(), ft[s].end(), by_cost);
+    std::stable_sort(at[s].begin(), at[s].end(), by_cost);
+    P->fwd[s] = Range{(int32_t)fwd_all.size(), (int32_t)ft[s].size()};
+    for (auto &x : ft[s]) fwd_all.push_back(x.second);
+    P->adj[s] = Range{(int32_t)adj_all.size(), (int32_t)at[s].size()};
+    for (auto &x : at[s]) adj_all.push_back(x.second);
+  }
+
+  // ------------------------------------------------ adjoint group-sum pieces
+  // Readers: every materialised block's input segments.  For a source range
+  // (c or a producer's zpool slot) the adjoint input is the sum of all reader
+  // partials that cover it.
+  struct Rd {
+    int32_t src;
+    int64_t start, len, pstart;
+  };
+  std::vector<Rd> readers;
+  for (const DevBlock &D : blocks) {
+    if (D.seg_len[0] > 0) readers.push_back({D.seg_src[0], D.seg_off[0], D.seg_len[0], D.part_off});
+    if (D.seg_len[1] > 0) readers.push_back({D.seg_src[1], D.seg_off[1], D.seg_len[1], D.part_off + D.seg_len[0]});
+  }
+  // producer regions: c = [0, m) ("stage -1"), zpool slots of stage s <= L
+  struct Region {
+    int32_t src, stage;
+    int64_t start, len;
+  };
+  std::vector<Region> regions;
+  regions.push_back({SRC_C, -1, 0, P->m});
+  for (int i = 0; i < (int)blocks.size(); ++i) {
+    const DevBlock &D = blocks[i];
+    if (!(D.flags & F_OUT_F) && D.r_out > 0) regions.push_back({SRC_Z, block_stage[i], D.out_off, D.r_out});
+  }
+  std::vector<std::vector<Piece>> pcs(L + 3);  // index stage+1 (0 = c)
+  std::vector<std::vector<std::vector<int64_t>>> pcs_rd(L + 3);
+  for (int src : {SRC_C, SRC_Z}) {
+    std::vector<int64_t> cuts;
+    std::vector<const Region *> regs;
+    for (const Region &g : regions)
+      if (g.src == src) {
+        regs.push_back(&g);
+        cuts.push_back(g.start);
+        cuts.push_back(g.start + g.len);
+      }
+    std::vector<int> rids;
+    for (int i = 0; i < (int)readers.size(); ++i)
+      if (readers[i].src == src) {
+        rids.push_back(i);
+        cuts.push_back(readers[i].start);
+        cuts.push_back(readers[i].start + readers[i].len);
+      }
+    std::sort(cuts.begin(), cuts.end());
+    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    std::sort(regs.begin(), regs.end(), [](const Region *a, const Region *b) { return a->start < b->start; });
+    // events sorted by coordinate
+    std::vector<std::pair<int64_t, int>> starts, ends;
+    for (int i : rids) {
+      starts.push_back({readers[i].start, i});
+      ends.push_back({readers[i].start + readers[i].len, i});
+    }
+    std::sort(starts.begin(), starts.end());
+    std::sort(ends.begin(), ends.end());
+    std::set<int> active;
+    size_t si = 0, ei = 0, ri = 0;
+    for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+      const int64_t a = cuts[k], e = cuts[k + 1];
+      while (ei < ends.size() && ends[ei].first <= a) active.erase(ends[ei++].second);
+      while (si < starts.size() && starts[si].first <= a) {
+        if (readers[starts[si].second].start + readers[starts[si].second].len > a) active.insert(starts[si].second);
+        ++si;
+      }
+      while (ri < regs.size() && regs[ri]->start + regs[ri]->len <= a) ++ri;
+      if (ri >= regs.size() || regs[ri]->start > a) {
+        if (!active.empty()) return fail(MHT_ERR_FORMAT, "reader outside any producer region");
+        continue;
+      }
+      const int slot = regs[ri]->stage + 1;
+      for (int64_t c0 = a; c0 < e; c0 += 1024) {
+        Piece pc;
+        memset(&pc, 0, sizeof pc);
+        pc.dst_src = src;
+        pc.dst_off = c0;
+        pc.len = (int32_t)std::min<int64_t>(1024, e - c0);
+        std::vector<int64_t> rr;
+        for (int id : active) rr.push_back(readers[id].pstart + (c0 - readers[id].start));
+        pc.rd_count = (int32_t)rr.size();
+        pcs[slot].push_back(pc);
+        pcs_rd[slot].push_back(std::move(rr));
+      }
+    }
+  }
+  std::vector<Piece> pieces_all;
+  std::vector<int64_t> rd_all;
+  P->pieces.assign(L + 2, Range{});
+  for (int slot = 0; slot < L + 3; ++slot) {
+    Range rg{(int32_t)pieces_all.size(), (int32_t)pcs[slot].size()};
+    for (size_t k = 0; k < pcs[slot].size(); ++k) {
+      Piece pc = pcs[slot][k];
+      pc.rd_begin = (int64_t)rd_all.size();
+      rd_all.insert(rd_all.end(), pcs_rd[slot][k].begin(), pcs_rd[slot][k].end());
+      pieces_all.push_back(pc);
+    }
+    if (slot == 0)
+      P->cpieces = rg;
+    else
+      P->pieces[slot - 1] = rg;
+  }
+
+  // ------------------------------------------------ upload
+  mht_status st;
+  if ((st = upload(&P->d_idx, idx_all, P->device_bytes)) != MHT_OK) return st;
+  if ((st = upload(&P->d_perm, perm, P->device_bytes)) != MHT_OK) return st;
+  if ((st = upload(&P->d_blocks, blocks, P->device_bytes)) != MHT_OK) return st;
+  if ((st = upload(&P->d_fwd, fwd_all, P->device_bytes)) != MHT_OK) return st;
+  if ((st = upload(&P->d_adj, adj_all, P->device_bytes)) != MHT_OK) return st;
+  if ((st = upload(&P->d_pieces, pieces_all, P->device_bytes)) != MHT_OK) return st;
+  if ((st = upload(&P->d_rd, rd_all, P->device_bytes)) != MHT_OK) return st;
+  return MHT_OK;
+}
+
+mht_status ensure_ws(mht_plan *P, int nrhs) {
+  if (nrhs <= P->ws_nrhs) return MHT_OK;
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  if (P->d_z) cudaFree(P->d_z);
+  if (P->d_part) cudaFree(P->d_part);
+  P->d_z = P->d_part = nullptr;
+  P->ws_nrhs = 0;
+  CUDA_TRY(cudaMalloc(&P->d_z, (size_t)P->Zt * nrhs * P->ssz));
+  CUDA_TRY(cudaMalloc(&P->d_part, (size_t)P->Pt * nrhs * P->ssz));
+  P->ws_nrhs = nrhs;
+  return MHT_OK;
+}
+
+Ctx make_ctx(mht_plan *P, int nrhs) {
+  Ctx cx;
+  memset(&cx, 0, sizeof cx);
+  cx.coef = P->d_coef;
+  cx.idx = P->d_idx;
+  cx.perm = P->d_perm;
+  cx.blocks = P->d_blocks;
+  cx.z = P->d_z;
+  cx.part = P->d_part;
+  cx.m = P->m;
+  cx.n = P->n;
+  cx.Zt = P->Zt;
+  cx.Pt = P->Pt;
+  cx.nrhs = nrhs;
+  return cx;
+}
+
+mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs) {
+  Ctx cx = make_ctx(P, nrhs);
+  cx.c = c;
+  cx.fout = f;
+  for (int s = 0; s < P->L + 2; ++s)
+    launch_fwd(P->cplx, cx, P->d_fwd + P->fwd[s].off, P->fwd[s].count, P->stream);
+  CUDA_TRY(cudaGetLastError());
+  return MHT_OK;
+}
+
+mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
+  Ctx cx = make_ctx(P, nrhs);
+  cx.fin = f;
+  cx.cw = c;
+  const int L = P->L;
+  launch_adj(P->cplx, cx, P->d_adj + P->adj[L + 1].off, P->adj[L + 1].count, true, P->stream);
+  for (int s = L; s >= 0; --s) {
+    launch_reduce(P->cplx, cx, P->d_pieces + P->pieces[s].off, P->d_rd, P->pieces[s].count, P->stream);
+    launch_adj(P->cplx, cx, P->d_adj + P->adj[s].off, P->adj[s].count, false, P->stream);
+  }
+  launch_reduce(P->cplx, cx, P->d_pieces + P->cpieces.off, P->d_rd, P->cpieces.count, P->stream);
+  CUDA_TRY(cudaGetLastError());
+  return MHT_OK;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+mht_status mht_plan_load(const char *path, int device, mht_plan **out) {
+  if (!path || !out) return fail(MHT_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  try {
+    std::unique_ptr<mht_plan> P(new mht_plan());
+    mht_status s = load_impl(path, device, P);
+    if (s != MHT_OK) return s;
+    *out = P.release();
+    return MHT_OK;
+  } catch (const std::bad_alloc &) {
+    return fail(MHT_ERR_OOM, "host allocation failed");
+  } catch (...) {
+    return fail(MHT_ERR_CUDA, "unexpected exception in loader");
+  }
+}
+
+mht_status mht_plan_info_get(const mht_plan *P, mht_plan_info *info) {
+  if (!P || !info) return fail(MHT_ERR_INVALID_ARG, "null argument");
+  memset(info, 0, sizeof *info);
+  info->n = P->n;
+  info->m = P->m;
+  info->L = P->L;
+  info->dtype = P->cplx ? MHT_DTYPE_C128 : MHT_DTYPE_F64;
+  info->tol = P->tol;
+  info->plan_bytes = P->plan_bytes;
+  info->factor_entries = P->factor_entries;
+  info->device_bytes = P->device_bytes;
+  info->index_entries = P->index_entries;
+  info->n_materialized = P->n_mat;
+  info->n_alias = P->n_alias;
+  int f = 0, a = 0;
+  for (int s = 0; s < P->L + 2; ++s) {
+    f += P->fwd[s].count > 0;
+    a += (P->adj[s].count > 0) + (s <= P->L && P->pieces[s].count > 0);
+  }
+  a += P->cpieces.count > 0;
+  info->fwd_launches = f;
+  info->adj_launches = a;
+  return MHT_OK;
+}
+
+mht_status mht_plan_set_stream(mht_plan *P, void *stream) {
+  if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
+  // keep our own non-blocking stream for loading; apply on the caller's stream
+  P->stream = static_cast<cudaStream_t>(stream);
+  return MHT_OK;
+}
+
+mht_status mht_reserve(mht_plan *P, int nrhs) {
+  if (!P || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  return ensure_ws(P, nrhs);
+}
+
+mht_status mht_apply(mht_plan *P, const void *c, void *f, int nrhs) {
+  if (!P || !c || !f || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s = ensure_ws(P, nrhs);
+  if (s != MHT_OK) return s;
+  return run_forward(P, c, f, nrhs);
+}
+
+mht_status mht_apply_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
+  if (!P || !c || !f || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s = ensure_ws(P, nrhs);
+  if (s != MHT_OK) return s;
+  return run_adjoint(P, f, c, nrhs);
+}
+
+static mht_status ensure_host_staging(mht_plan *P, int nrhs) {
+  if (nrhs <= P->host_nrhs) return MHT_OK;
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  if (P->d_hc) cudaFree(P->d_hc);
+  if (P->d_hf) cudaFree(P->d_hf);
+  P->d_hc = P->d_hf = nullptr;
+  P->host_nrhs = 0;
+  CUDA_TRY(cudaMalloc(&P->d_hc, (size_t)P->m * nrhs * P->ssz));
+  CUDA_TRY(cudaMalloc(&P->d_hf, (size_t)P->n * nrhs * P->ssz));
+  P->host_nrhs = nrhs;
+  return MHT_OK;
+}
+
+mht_status mht_apply_host(mht_plan *P, const void *c_host, void *f_host, int nrhs) {
+  if (!P || !c_host || !f_host || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s;
+  if ((s = ensure_ws(P, nrhs)) != MHT_OK || (s = ensure_host_staging(P, nrhs)) != MHT_OK) return s;
+  CUDA_TRY(cudaMemcpyAsync(P->d_hc, c_host, (size_t)P->m * nrhs * P->ssz, cudaMemcpyHostToDevice, P->stream));
+  if ((s = run_forward(P, P->d_hc, P->d_hf, nrhs)) != MHT_OK) return s;
+  CUDA_TRY(cudaMemcpyAsync(f_host, P->d_hf, (size_t)P->n * nrhs * P->ssz, cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  return MHT_OK;
+}
+
+mht_status mht_apply_adjoint_host(mht_plan *P, const void *f_host, void *c_host, int nrhs) {
+  if (!P || !c_host || !f_host || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s;
+  if ((s = ensure_ws(P, nrhs)) != MHT_OK || (s = ensure_host_staging(P, nrhs)) != MHT_OK) return s;
+  CUDA_TRY(cudaMemcpyAsync(P->d_hf, f_host, (size_t)P->n * nrhs * P->ssz, cudaMemcpyHostToDevice, P->stream));
+  if ((s = run_adjoint(P, P->d_hf, P->d_hc, nrhs)) != MHT_OK) return s;
+  CUDA_TRY(cudaMemcpyAsync(c_host, P->d_hc, (size_t)P->m * nrhs * P->ssz, cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  return MHT_OK;
+}
+
+mht_status mht_set_graphs(mht_plan *P, int on) {
+  if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
+  P->graphs = on != 0;
+  return MHT_OK;
+}
+
+mht_status mht_sync(mht_plan *P) {
+  if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
+  CUDA_TRY(cudaSetDevice(P->device));
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  CUDA_TRY(cudaGetLastError());
+  return MHT_OK;
+}
+
+mht_status mht_stage_stats(const mht_plan *P, int stage, int64_t *coef_bytes, int32_t *n_mat,
+                           int32_t *n_tiles_fwd, int32_t *n_tiles_adj) {
+  if (!P || stage < 0 || stage > P->L + 1) return fail(MHT_ERR_INVALID_ARG, "bad stage");
+  if (coef_bytes) *coef_bytes = P->stage_coef_bytes[stage];
+  if (n_mat) *n_mat = P->stage_nmat[stage];
+  if (n_tiles_fwd) *n_tiles_fwd = P->fwd[stage].count;
+  if (n_tiles_adj) *n_tiles_adj = P->adj[stage].count;
+  return MHT_OK;
+}
+
+void mht_plan_destroy(mht_plan *P) {
+  if (!P) return;
+  cudaSetDevice(P->device);
+  delete P;
+}
+
+const char *mht_status_string(mht_status s) {
+  switch (s) {
+    case MHT_OK: return "MHT_OK";
+    case MHT_ERR_INVALID_ARG: return "MHT_ERR_INVALID_ARG";
+    case MHT_ERR_FORMAT: return "MHT_ERR_FORMAT";
+    case MHT_ERR_SHAPE: return "MHT_ERR_SHAPE";
+    case MHT_ERR_OOM: return "MHT_ERR_OOM";
+    case MHT_ERR_CUDA: return "MHT_ERR_CUDA";
+    case MHT_ERR_UNSUPPORTED: return "MHT_ERR_UNSUPPORTED";
+    case MHT_ERR_IO: return "MHT_ERR_IO";
+  }
+  return "MHT_ERR_UNKNOWN";
+}
+
+const char *mht_last_error(void) { return g_err.c_str(); }
+
+const char *mht_build_info(void) { return "libmht sm_100a fp64 butterfly MHT apply (v1)"; }
+
+}  // extern "C"

@@ -1,0 +1,224 @@
+"""Thin Python binding of libmht (include/mht.h) — argument marshalling only.
+
+Every step of the transform runs in the CUDA kernels of ``libmht.so``; this
+module only checks tensor shapes/dtypes/devices and passes raw pointers and
+torch's current stream through ctypes.  There is no CPU fallback: if the
+extension is missing or no B200 is present, the calls raise.
+
+Names follow the C ABI: ``mht_plan_load``, ``mht_apply``, ``mht_apply_adjoint``,
+``mht_apply_host``, ``mht_apply_adjoint_host``, ``mht_plan_info_get``, ...
+``Plan`` wraps them for convenience.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmht.so")
+
+MHT_DTYPE_F64, MHT_DTYPE_C128 = 1, 2
+EXPORTED = [
+    "mht_plan_load", "mht_plan_info_get", "mht_plan_set_stream", "mht_reserve", "mht_apply",
+    "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host", "mht_set_graphs", "mht_sync",
+    "mht_stage_stats", "mht_plan_destroy", "mht_status_string", "mht_last_error", "mht_build_info",
+]
+
+
+class MhtError(RuntimeError):
+    pass
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("n", C.c_int64), ("m", C.c_int64), ("L", C.c_int32), ("dtype", C.c_int32),
+                ("tol", C.c_double), ("plan_bytes", C.c_int64), ("factor_entries", C.c_int64),
+                ("device_bytes", C.c_int64), ("index_entries", C.c_int64),
+                ("n_materialized", C.c_int32), ("n_alias", C.c_int32),
+                ("fwd_launches", C.c_int32), ("adj_launches", C.c_int32)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """dlopen libmht.so (raises if it has not been built — no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise MhtError(f"{path} not found: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(path)
+    vp, i32, i64 = C.c_void_p, C.c_int, C.c_int64
+    L.mht_plan_load.argtypes = [C.c_char_p, i32, C.POINTER(vp)]
+    L.mht_plan_info_get.argtypes = [vp, C.POINTER(PlanInfo)]
+    L.mht_plan_set_stream.argtypes = [vp, vp]
+    L.mht_reserve.argtypes = [vp, i32]
+    for nm in ("mht_apply", "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host"):
+        getattr(L, nm).argtypes = [vp, vp, vp, i32]
+    L.mht_set_graphs.argtypes = [vp, i32]
+    L.mht_sync.argtypes = [vp]
+    L.mht_stage_stats.argtypes = [vp, i32, C.POINTER(i64), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_int32)]
+    L.mht_plan_destroy.argtypes = [vp]
+    L.mht_plan_destroy.restype = None
+    L.mht_status_string.argtypes = [i32]
+    L.mht_status_string.restype = C.c_char_p
+    L.mht_last_error.restype = C.c_char_p
+    L.mht_build_info.restype = C.c_char_p
+    for nm in EXPORTED:
+        if nm not in ("mht_plan_destroy", "mht_status_string", "mht_last_error", "mht_build_info"):
+            getattr(L, nm).restype = i32
+    _lib = L
+    return L
+
+
+def _check(st: int, what: str):
+    if st != 0:
+        L = load_library()
+        raise MhtError(f"{what}: {L.mht_status_string(st).decode()}: {L.mht_last_error().decode()}")
+
+
+# ------------------------------------------------------------ C-named calls
+def mht_plan_load(path: str, device: int = 0) -> int:
+    L = load_library()
+    h = C.c_void_p()
+    _check(L.mht_plan_load(str(path).encode(), int(device), C.byref(h)), "mht_plan_load")
+    return h.value
+
+
+def mht_plan_info_get(plan: int) -> PlanInfo:
+    info = PlanInfo()
+    _check(load_library().mht_plan_info_get(plan, C.byref(info)), "mht_plan_info_get")
+    return info
+
+
+def mht_plan_set_stream(plan: int, stream_ptr: int):
+    _check(load_library().mht_plan_set_stream(plan, C.c_void_p(stream_ptr)), "mht_plan_set_stream")
+
+
+def _dev_ptr(t, rows: int, nrhs: int, dt):
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise MhtError("expected a CUDA tensor")
+    if t.dtype != dt or not t.is_contiguous() or t.numel() != rows * nrhs:
+        raise MhtError(f"expected contiguous {dt} tensor with {rows}*{nrhs} elements, got "
+                       f"{t.dtype} {tuple(t.shape)}")
+    return C.c_void_p(t.data_ptr())
+
+
+def mht_apply(plan: int, c, f, nrhs: int, n: int, m: int, dt):
+    _check(load_library().mht_apply(plan, _dev_ptr(c, m, nrhs, dt), _dev_ptr(f, n, nrhs, dt), int(nrhs)),
+           "mht_apply")
+
+
+def mht_apply_adjoint(plan: int, f, c, nrhs: int, n: int, m: int, dt):
+    _check(load_library().mht_apply_adjoint(plan, _dev_ptr(f, n, nrhs, dt), _dev_ptr(c, m, nrhs, dt),
+                                            int(nrhs)), "mht_apply_adjoint")
+
+
+def mht_plan_destroy(plan: int):
+    load_library().mht_plan_destroy(plan)
+
+
+# ------------------------------------------------------------ convenience
+class Plan:
+    """A loaded plan on one GPU.  Vectors are (nrhs, m) / (nrhs, n) tensors
+    (= column-major m x nrhs / n x nrhs, the ABI layout)."""
+
+    def __init__(self, path: str, device: int = 0):
+        import torch
+
+        self.device = torch.device("cuda", device)
+        self._h = mht_plan_load(path, device)
+        self.info = mht_plan_info_get(self._h)
+        self.n, self.m, self.L = self.info.n, self.info.m, self.info.L
+        self.is_complex = self.info.dtype == MHT_DTYPE_C128
+        self.torch_dtype = torch.complex128 if self.is_complex else torch.float64
+        self.np_dtype = np.complex128 if self.is_complex else np.float64
+        self.scalar_bytes = 16 if self.is_complex else 8
+
+    def _stream(self):
+        import torch
+
+        mht_plan_set_stream(self._h, torch.cuda.current_stream(self.device).cuda_stream)
+
+    def reserve(self, nrhs: int):
+        _check(load_library().mht_reserve(self._h, int(nrhs)), "mht_reserve")
+
+    def apply(self, c, out=None):
+        import torch
+
+        c2 = c.reshape(-1, self.m) if c.dim() != 2 else c
+        nrhs = c2.shape[0]
+        f = out if out is not None else torch.empty((nrhs, self.n), dtype=self.torch_dtype, device=self.device)
+        self._stream()
+        mht_apply(self._h, c2, f, nrhs, self.n, self.m, self.torch_dtype)
+        return f
+
+    def adjoint(self, f, out=None):
+        import torch
+
+        f2 = f.reshape(-1, self.n) if f.dim() != 2 else f
+        nrhs = f2.shape[0]
+        c = out if out is not None else torch.empty((nrhs, self.m), dtype=self.torch_dtype, device=self.device)
+        self._stream()
+        mht_apply_adjoint(self._h, f2, c, nrhs, self.n, self.m, self.torch_dtype)
+        return c
+
+    def apply_host(self, c_host: np.ndarray, f_host: np.ndarray | None = None):
+        """End-to-end call from host memory (pinned for full bandwidth)."""
+        c_host = np.ascontiguousarray(c_host, dtype=self.np_dtype).reshape(-1, self.m)
+        nrhs = c_host.shape[0]
+        if f_host is None:
+            f_host = np.empty((nrhs, self.n), dtype=self.np_dtype)
+        self._stream()
+        _check(load_library().mht_apply_host(self._h, C.c_void_p(c_host.ctypes.data),
+                                             C.c_void_p(f_host.ctypes.data), nrhs), "mht_apply_host")
+        return f_host
+
+    def adjoint_host(self, f_host: np.ndarray, c_host: np.ndarray | None = None):
+        f_host = np.ascontiguousarray(f_host, dtype=self.np_dtype).reshape(-1, self.n)
+        nrhs = f_host.shape[0]
+        if c_host is None:
+            c_host = np.empty((nrhs, self.m), dtype=self.np_dtype)
+        self._stream()
+        _check(load_library().mht_apply_adjoint_host(self._h, C.c_void_p(f_host.ctypes.data),
+                                                     C.c_void_p(c_host.ctypes.data), nrhs),
+               "mht_apply_adjoint_host")
+        return c_host
+
+    def apply_host_ptr(self, c_ptr: int, f_ptr: int, nrhs: int):
+        self._stream()
+        _check(load_library().mht_apply_host(self._h, C.c_void_p(c_ptr), C.c_void_p(f_ptr), nrhs), "mht_apply_host")
+
+    def adjoint_host_ptr(self, f_ptr: int, c_ptr: int, nrhs: int):
+        self._stream()
+        _check(load_library().mht_apply_adjoint_host(self._h, C.c_void_p(f_ptr), C.c_void_p(c_ptr), nrhs),
+               "mht_apply_adjoint_host")
+
+    def sync(self):
+        _check(load_library().mht_sync(self._h), "mht_sync")
+
+    def stage_stats(self):
+        out = []
+        for s in range(self.L + 2):
+            cb = C.c_int64()
+            nm, tf, ta = C.c_int32(), C.c_int32(), C.c_int32()
+            _check(load_library().mht_stage_stats(self._h, s, C.byref(cb), C.byref(nm), C.byref(tf), C.byref(ta)),
+                   "mht_stage_stats")
+            out.append(dict(stage=s, coef_bytes=cb.value, n_mat=nm.value, fwd_tiles=tf.value, adj_tiles=ta.value))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            mht_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,198 @@
+"""GPU parity: libmht (CUDA, through the C ABI) vs the oracle (CPU).
+
+Bars (BASELINE.json north_star): relative l2 <= 1e-12 against the oracle's
+independent butterfly apply O2 on the same plan, and <= 10 x the ID tolerance
+against the dense sum O1, per column (reading A17).  Plans span several tiles
+(64-row forward tiles, 32-column adjoint tiles) with ragged tails; edge cases
+cover zero input, rank-0 / rank-1 matrices (COPY, alias and empty blocks),
+ragged leaves, L = 0, multi-RHS widths that are not multiples of the register
+blocking, the host-buffer API, determinism and corrupt plan files.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import mht_inputs as mi
+from paper_2605_21828_b200 import workloads as W
+from paper_2605_21828_b200.precompute import build_plan, freq_tree, kd_tree
+from paper_2605_21828_b200.precompute.basis import DenseBasis
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+PARITY = 1e-12
+
+
+def rel_cols(a, b):
+    a = np.atleast_2d(a)
+    b = np.atleast_2d(b)
+    out = []
+    for r in range(a.shape[0]):
+        nb = np.linalg.norm(b[r])
+        out.append(np.linalg.norm(a[r] - b[r]) / (nb if nb > 0 else 1.0))
+    return max(out)
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a GPU")
+    from paper_2605_21828_b200 import _build, mht
+
+    _build.build()
+    mht.load_library()
+    return mht
+
+
+@pytest.fixture(scope="module")
+def plans(tmp_path_factory):
+    return tmp_path_factory.mktemp("gpu_plans")
+
+
+def flat_case(plans, n, side, L, tol, m=None, name="f"):
+    w = W.flat_workload(n, side, L, tol, name=name)
+    if m is not None:
+        w = mi.Workload(name, "flat", n, m, "complex128", tol, L, (1,), {"side": side})
+    path = str(plans / f"{name}_{n}_{side}_{L}_{tol:g}_{w.m}.plan")
+    if not os.path.exists(path):
+        W.build_workload_plan(w, path, workers=8, log=None)
+    return path, w
+
+
+def check_plan(gpu, oracle_lib, path, w, nrhs_list=(1,), dense=None):
+    P = gpu.Plan(path)
+    O = oracle_lib.Plan(path)
+    for nrhs in nrhs_list:
+        if w.dtype == "complex128":
+            c = mi.complex_gaussian(nrhs, w.m, 100 + nrhs)
+            y = mi.complex_gaussian(nrhs, w.n, 200 + nrhs)
+        else:
+            c = mi.real_gaussian(nrhs, w.m, 100 + nrhs)
+            y = mi.real_gaussian(nrhs, w.n, 200 + nrhs)
+        f = P.apply(torch.from_numpy(c).cuda()).cpu().numpy()
+        ca = P.adjoint(torch.from_numpy(y).cuda()).cpu().numpy()
+        assert rel_cols(f, O.apply(c)) <= PARITY, ("fwd", nrhs)
+        assert rel_cols(ca, O.adjoint(y)) <= PARITY, ("adj", nrhs)
+        if dense is not None:
+            fd, cd = dense(c, y)
+            assert rel_cols(f, fd) <= 10 * w.tol, ("fwd dense", nrhs, rel_cols(f, fd))
+            assert rel_cols(ca, cd) <= 10 * w.tol, ("adj dense", nrhs, rel_cols(ca, cd))
+    return P, O
+
+
+def flat_dense(oracle_lib, w):
+    x = mi.flat_points(w.n)
+    k = mi.flat_modes(w.extra["side"])[: w.m]
+    return lambda c, y: (oracle_lib.flat_synth(x, k, c), oracle_lib.flat_analysis(x, k, y))
+
+
+def test_flat_small_parity(gpu, oracle_lib, plans):
+    path, w = flat_case(plans, 2048, 32, 4, 1e-8)
+    check_plan(gpu, oracle_lib, path, w, (1, 2, 3, 5, 8, 32), dense=flat_dense(oracle_lib, w))
+
+
+def test_flat_loose_tolerance_compressed(gpu, oracle_lib, plans):
+    path, w = flat_case(plans, 4096, 32, 5, 1e-4)
+    P, O = check_plan(gpu, oracle_lib, path, w, (1, 7), dense=flat_dense(oracle_lib, w))
+    assert P.info.factor_entries < w.n * w.m
+
+
+def test_config1_full_parity(gpu, oracle_lib, plans):
+    """configs[0]: n = m = 4096, k in [-32,31]^2, tol 1e-8, nrhs 1, all rows."""
+    w = mi.WORKLOADS["c1"]
+    path = str(plans / "c1.plan")
+    W.build_workload_plan(w, path, workers=8, log=None)
+    check_plan(gpu, oracle_lib, path, w, (1, 4), dense=flat_dense(oracle_lib, w))
+
+
+def test_sphere_parity(gpu, oracle_lib, plans):
+    lmax = 31
+    w = W.sphere_workload(2048, lmax, 4, 1e-10)
+    path = str(plans / "sph.plan")
+    W.build_workload_plan(w, path, workers=8, log=None)
+    th, ph, _ = mi.sphere_points(w.n)
+    dense = lambda c, y: (oracle_lib.sphere_synth(th, ph, lmax, c), oracle_lib.sphere_analysis(th, ph, lmax, y))
+    check_plan(gpu, oracle_lib, path, w, (1, 3, 32), dense=dense)
+
+
+def test_ragged_leaves_and_L0(gpu, oracle_lib, plans):
+    path, w = flat_case(plans, 1000, 32, 4, 1e-9, m=1000, name="ragged")
+    check_plan(gpu, oracle_lib, path, w, (1, 3), dense=flat_dense(oracle_lib, w))
+    path0, w0 = flat_case(plans, 64, 8, 0, 1e-12, name="L0")
+    check_plan(gpu, oracle_lib, path0, w0, (1, 2), dense=flat_dense(oracle_lib, w0))
+
+
+def test_full_rank_plan_identity_copy_paths(gpu, oracle_lib, plans):
+    """tol ~ 0: many IDENTITY blocks -> alias and COPY resolution paths."""
+    path, w = flat_case(plans, 1024, 32, 4, 1e-15, name="exact")
+    P, _ = check_plan(gpu, oracle_lib, path, w, (1, 4), dense=flat_dense(oracle_lib, w))
+    assert P.info.n_alias > 0
+
+
+def _dense_plan(plans, Phi, L, tol, name):
+    n, m = Phi.shape
+    pts = np.random.default_rng(0).uniform(size=(n, 2))
+    perm, sp_off = kd_tree(pts, L)
+    path = str(plans / f"{name}.plan")
+    build_plan(DenseBasis(Phi), perm, sp_off, freq_tree(m, L), L, tol, path, workers=1, log=None)
+    return path
+
+
+def test_rank0_rank1_and_exact_zero(gpu, oracle_lib, plans):
+    rng = np.random.default_rng(4)
+    u, v = rng.standard_normal(512), rng.standard_normal(512)
+    w = mi.Workload("r1", "mesh", 512, 512, "float64", 1e-12, 3)
+    p1 = _dense_plan(plans, np.outer(u, v), 3, 1e-12, "gpu_rank1")
+    check_plan(gpu, oracle_lib, p1, w, (1, 5))
+    p0 = _dense_plan(plans, np.zeros((512, 512)), 3, 1e-12, "gpu_rank0")
+    P0 = gpu.Plan(p0)
+    c = torch.from_numpy(rng.standard_normal((2, 512))).cuda()
+    assert torch.count_nonzero(P0.apply(c)).item() == 0
+    assert torch.count_nonzero(P0.adjoint(c)).item() == 0
+    # c = 0 -> f = 0 exactly, and y = 0 -> 0
+    path, wf = flat_case(plans, 2048, 32, 4, 1e-8)
+    P = gpu.Plan(path)
+    z = torch.zeros((1, wf.m), dtype=torch.complex128, device="cuda")
+    assert torch.count_nonzero(P.apply(z)).item() == 0
+    assert torch.count_nonzero(P.adjoint(torch.zeros((1, wf.n), dtype=torch.complex128, device="cuda"))).item() == 0
+
+
+def test_determinism_and_host_api(gpu, oracle_lib, plans):
+    path, w = flat_case(plans, 2048, 32, 4, 1e-8)
+    P = gpu.Plan(path)
+    c = mi.complex_gaussian(3, w.m, 9)
+    y = mi.complex_gaussian(3, w.n, 10)
+    ct = torch.from_numpy(c).cuda()
+    yt = torch.from_numpy(y).cuda()
+    f1, f2 = P.apply(ct), P.apply(ct)
+    a1, a2 = P.adjoint(yt), P.adjoint(yt)
+    assert torch.equal(f1, f2) and torch.equal(a1, a2)  # no atomics: bitwise deterministic
+    fh = P.apply_host(c)
+    ah = P.adjoint_host(y)
+    assert np.array_equal(fh, f1.cpu().numpy()) and np.array_equal(ah, a1.cpu().numpy())
+
+
+def test_adjoint_identity_gpu(gpu, oracle_lib, plans):
+    path, w = flat_case(plans, 2048, 32, 4, 1e-8)
+    P = gpu.Plan(path)
+    c = torch.from_numpy(mi.complex_gaussian(1, w.m, 1)).cuda()
+    y = torch.from_numpy(mi.complex_gaussian(1, w.n, 2)).cuda()
+    lhs = torch.vdot(y[0], P.apply(c)[0]).item()
+    rhs = torch.vdot(P.adjoint(y)[0], c[0]).item()
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs) * 10
+
+
+def test_corrupt_plan_rejected(gpu, plans):
+    path, w = flat_case(plans, 2048, 32, 4, 1e-8)
+    raw = bytearray(open(path, "rb").read())
+    raw[len(raw) // 2] ^= 0x40
+    bad = str(plans / "corrupt.plan")
+    open(bad, "wb").write(raw)
+    with pytest.raises(gpu.MhtError, match="FORMAT"):
+        gpu.Plan(bad)
+    with pytest.raises(gpu.MhtError, match="IO"):
+        gpu.Plan(str(plans / "missing.plan"))
+    P = gpu.Plan(path)
+    with pytest.raises(gpu.MhtError):
+        P.apply(torch.zeros((1, w.m + 1), dtype=torch.complex128, device="cuda"))
