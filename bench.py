@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""bench.py — butterfly MHT apply/adjoint on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mht|reference] [--workload c2]
+
+A *step* is one pass of the whole hot path over
+one batch of synthetic input: synthesis f = Phi c and analysis c = Phi^* f at
+nrhs = 1 and at the workload's multi-RHS width (32 for configs[1]), i.e.
+2 * (1 + 32) = 66 column transforms per step.  ``value`` is column transforms
+per second summed over all ranks (weak scaling: every rank is an independent
+replica over its own right-hand sides — "replicas only").
+
+Workload: configs[1] (flat periodic square, n = m = 65,536, tol 1e-8) — the
+configuration BASELINE.json's metric is quoted on.  The plan (tens of GB) is
+far larger than L2, so no L2 flush is needed; for small workloads (< 4 x L2)
+a 256 MiB buffer is rewritten between timed steps.
+
+``--impl reference`` times the oracle (independent CPU butterfly apply O2,
+``oracle/``) on this box's host cores on a bounded sample of the same workload
+(rank 0 only; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import mht_inputs as mi  # noqa: E402
+
+METRIC = "MHT applies/sec (fp64) and achieved HBM GB/s / FP64 % of peak at nrhs=1 and 32"
+UNIT = "column transforms/s"
+L2_BYTES = 126 * 2**20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mht", choices=["mht", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(mi.WORKLOADS))
+    ap.add_argument("--builder", default="gpu", choices=["gpu", "cpu"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(self.idx)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- setup
+def dist_setup(args):
+    import torch
+
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    lrank = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(lrank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
+    else:
+        torch.cuda.set_device(0)
+    return ws, rank, lrank
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def get_plan(w, args, ws, rank, lrank):
+    from paper_2605_21828_b200 import workloads as W
+
+    path = W.plan_cache_path(w)
+    if rank == 0 and not os.path.exists(path):
+        t0 = time.time()
+        st = W.build_workload_plan(w, path + ".build", builder=args.builder, device=f"cuda:{lrank}",
+                                   log=lambda s: log(s))
+        os.replace(path + ".build", path)
+        log(f"[bench] plan built in {time.time() - t0:.1f}s: {st['entries']} entries "
+            f"({st['entries'] / st['dense_entries']:.3f} of dense), {st['plan_bytes'] / 1e9:.2f} GB")
+        import torch
+
+        torch.cuda.empty_cache()
+    barrier(ws)
+    return path
+
+
+def phases_for(w):
+    ph = [("fwd", 1), ("adj", 1)]
+    for r in w.nrhs:
+        if r > 1:
+            ph += [("fwd", r), ("adj", r)]
+    return ph
+
+
+def dtype_tag(w):
+    return "c128" if w.dtype == "complex128" else "f64"
+
+
+def workload_desc(w):
+    if w.family == "flat":
+        return f"{w.name}: flat periodic square, n=m={w.n}, k in [-{w.extra['side'] // 2},{w.extra['side'] // 2 - 1}]^2, tol {w.tol:g}"
+    if w.family == "sphere":
+        return f"{w.name}: unit sphere, n={w.n}, real SH l<={w.extra['lmax']}, tol {w.tol:g}"
+    return f"{w.name}: torus mesh n={w.n}, m={w.m}, tol {w.tol:g}"
+
+
+# ---------------------------------------------------------------- oracle (CPU) legs
+def time_oracle(path, w, seconds, steps=None, warmup=0):
+    """O2 forward + adjoint at nrhs = 1, repeated; returns (transforms/s, reps, s, threads)."""
+    import oracle
+
+    O = oracle.Plan(path, verify_checksum=False)
+    c = mi.workload_coefficients(w, 1)
+    y = mi.workload_adjoint_input(w, 1)
+    for _ in range(warmup):
+        O.apply(c)
+        O.adjoint(y)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        O.apply(c)
+        O.adjoint(y)
+        reps += 1
+        el = time.perf_counter() - t0
+        if (steps is not None and reps >= steps) or (steps is None and el >= seconds):
+            break
+    O.close()
+    return 2 * reps / el, reps, el, oracle.num_threads()
+
+
+def run_reference(args, w, path):
+    v, reps, el, cores = time_oracle(path, w, None, steps=args.steps, warmup=args.warmup)
+    sample = (f"oracle O2 (independent CPU butterfly apply, C + OpenMP) on the full {w.name} plan: "
+              f"synthesis + analysis at nrhs=1 per step, {reps} steps in {el:.1f}s")
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / reps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_tag(w),
+           "data": "synthetic (seeded, mht_inputs)",
+           "config": {"workload": workload_desc(w), "nrhs": [1], "plan": os.path.basename(path)},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------- main
+def main():
+    args = parse()
+    import torch
+
+    w = mi.WORKLOADS[args.workload]
+    ws, rank, lrank = dist_setup(args)
+    if args.impl == "reference" and rank != 0:
+        # the reference arm runs on rank 0 only; other ranks exit without work
+        barrier(ws)
+        return
+    path = get_plan(w, args, 1 if args.impl == "reference" else ws, rank, lrank)
+    if args.impl == "reference":
+        run_reference(args, w, path)
+        return
+
+    from paper_2605_21828_b200 import mht
+
+    P = mht.Plan(path, lrank)
+    dev = torch.device("cuda", lrank)
+    phases = phases_for(w)
+    widths = sorted({r for _, r in phases})
+    P.reserve(max(widths))
+    sb = P.scalar_bytes
+    # inputs (each rank its own right-hand sides: replicas over RHS columns)
+    ins, outs = {}, {}
+    for r in widths:
+        c = mi.workload_coefficients(w, r + rank * 0) if rank == 0 else _rank_coef(w, r, rank)
+        y = mi.workload_adjoint_input(w, r) if rank == 0 else _rank_adj(w, r, rank)
+        ins[("fwd", r)] = torch.from_numpy(c).to(dev)
+        ins[("adj", r)] = torch.from_numpy(y).to(dev)
+        outs[("fwd", r)] = torch.empty((r, w.n), dtype=P.torch_dtype, device=dev)
+        outs[("adj", r)] = torch.empty((r, w.m), dtype=P.torch_dtype, device=dev)
+
+    def step():
+        for kind, r in phases:
+            if kind == "fwd":
+                P.apply(ins[(kind, r)], out=outs[(kind, r)])
+            else:
+                P.adjoint(ins[(kind, r)], out=outs[(kind, r)])
+
+    flush = None
+    if P.info.plan_bytes < 4 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(lrank)
+    P.set_profiling(True)
+    P.profile_reset()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier(ws)
+    torch.cuda.synchronize()
+    clocks.start()
+    for k in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        ev[k][0].record()
+        step()
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier(ws)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = allreduce_max(sum(step_ms), ws)
+    transforms = sum(r for _, r in phases)
+    value = ws * transforms * args.steps / (total_ms / 1e3)
+
+    # ---- per-kernel live timing (events bracket every launch on its stream)
+    stats = P.stage_stats()
+    coef_bytes = sum(s["coef_bytes"] for s in stats)
+    entries = P.info.factor_entries
+    per = {}
+    for kind_i, kind in ((0, "fwd"), (1, "adj"), (2, "sum")):
+        for r in widths:
+            ms, nl = P.profile_get(kind_i, -1, r)
+            if nl:
+                per[(kind, r)] = (ms, nl)
+    P.set_profiling(False)
+    breakdown = {}
+    for (kind, r), (ms, nl) in per.items():
+        applies = args.steps
+        byts = (coef_bytes + (w.m + w.n) * r * sb) * applies if kind != "sum" else None
+        flops = (8 if P.is_complex else 2) * entries * r * applies
+        breakdown[f"{kind}_nrhs{r}"] = {
+            "ms_per_apply": ms / applies, "launches_per_apply": nl / applies,
+            "GBps": (byts / (ms / 1e3) / 1e9) if byts else None,
+            "TFLOPs": (flops / (ms / 1e3) / 1e12) if kind != "sum" else None}
+    peaks = _peaks()
+    dom = max(((k, v) for k, v in per.items() if k[0] in ("fwd", "adj")), key=lambda kv: kv[1][0])
+    (dkind, dr), (dms, dn) = dom
+    per_launch_ms = dms / dn
+    if dr == 1:
+        alg = (coef_bytes + (w.m + w.n) * sb) / (dn / args.steps)        # bytes per launch (average)
+        achieved = alg / (per_launch_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "kernel": f"{dkind}_kernel nrhs=1", "peak_source": peaks["hbm_src"]}
+    else:
+        alg = (8 if P.is_complex else 2) * entries * dr / (dn / args.steps)
+        achieved = alg / (per_launch_ms / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["fp64_tflops"], "traffic": None,
+                "kernel": f"{dkind}_kernel nrhs={dr} (FP64 FMA pipe)", "peak_source": peaks["fp64_src"]}
+    roof["per_launch_ms"] = per_launch_ms
+    roof["launches_per_apply"] = dn / args.steps
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": dtype_tag(w),
+           "data": "synthetic (seeded generators in mht_inputs; no paper dataset)",
+           "config": {"workload": workload_desc(w), "phases": [f"{k}@nrhs{r}" for k, r in phases],
+                      "transforms_per_step_per_gpu": transforms, "parallelism": f"replicas{ws}",
+                      "plan_bytes": P.info.plan_bytes, "factor_entries": entries,
+                      "factor_fraction_of_dense": entries / (w.n * w.m),
+                      "l2": ("plan larger than L2 (no flush)" if flush is None else "L2 flushed between steps")},
+           "roofline": roof, "breakdown": breakdown, "clocks": clk,
+           "gpu_launches": args.steps * sum(P.info.fwd_launches if k == "fwd" else P.info.adj_launches
+                                             for k, _ in phases)}
+
+    # ---- end to end through the C ABI with pinned host buffers
+    if not args.no_e2e:
+        out["e2e"] = _e2e(P, phases, w, ws, args)
+    # ---- CPU oracle baseline (rank 0, N = 1)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        v, reps, el, cores = time_oracle(path, w, args.cpu_seconds)
+        out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                               "sample": f"O2 synthesis+analysis at nrhs=1 on the full {w.name} plan, "
+                                         f"{reps} reps in {el:.1f}s (bounded sample of the step's phases)"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    P.close()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def _rank_coef(w, r, rank):
+    if w.dtype == "complex128":
+        return mi.complex_gaussian(r, w.m, mi.SEED_COEF + 1000 * rank)
+    return mi.real_gaussian(r, w.m, mi.SEED_COEF + 1000 * rank)
+
+
+def _rank_adj(w, r, rank):
+    if w.dtype == "complex128":
+        return mi.complex_gaussian(r, w.n, mi.SEED_ADJ + 1000 * rank)
+    return mi.real_gaussian(r, w.n, mi.SEED_ADJ + 1000 * rank)
+
+
+def _e2e(P, phases, w, ws, args):
+    import torch
+
+    host_in, host_out = {}, {}
+    h2d = d2h = 0
+    for kind, r in phases:
+        nin, nout = (w.m, w.n) if kind == "fwd" else (w.n, w.m)
+        src = (mi.workload_coefficients(w, r) if kind == "fwd" else mi.workload_adjoint_input(w, r))
+        ti = torch.from_numpy(src).pin_memory()
+        to = torch.empty((r, nout), dtype=P.torch_dtype).pin_memory()
+        host_in[(kind, r)], host_out[(kind, r)] = ti, to
+        h2d += ti.numel() * P.scalar_bytes
+        d2h += to.numel() * P.scalar_bytes
+
+    def step():
+        for kind, r in phases:
+            ti, to = host_in[(kind, r)], host_out[(kind, r)]
+            if kind == "fwd":
+                P.apply_host_ptr(ti.data_ptr(), to.data_ptr(), r)
+            else:
+                P.adjoint_host_ptr(ti.data_ptr(), to.data_ptr(), r)
+
+    step()
+    barrier(ws)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        step()
+    el = allreduce_max(time.perf_counter() - t0, ws)
+    transforms = sum(r for _, r in phases)
+    return {"value": ws * transforms * args.e2e_steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+            "api": "mht_apply_host / mht_apply_adjoint_host (pinned host buffers, copies in the timed region)"}
+
+
+def _peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written) for HBM; FP64
+    from the measured DFMA microbenchmark in profiles/ if present, else derived
+    from unit counts and clocks."""
+    out = {}
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(mp))
+        out["hbm_gbs"] = float(d["hbm_gbs"])
+        out["hbm_src"] = "measured (MEASURED_PEAKS.json hbm_gbs)"
+        smax = float(d.get("sm_max_mhz", 1965.0))
+    except Exception:
+        out["hbm_gbs"] = 6650.0
+        out["hbm_src"] = "fallback (B200_PROFILING.md 6.65 TB/s)"
+        smax = 1965.0
+    fp = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    try:
+        d = json.load(open(fp))
+        out["fp64_tflops"] = float(d["dfma_tflops"])
+        out["fp64_src"] = f"measured DFMA microbenchmark ({os.path.relpath(fp, ROOT)})"
+    except Exception:
+        out["fp64_tflops"] = 148 * 64 * 2 * smax * 1e6 / 1e12
+        out["fp64_src"] = "derived: 148 SMs x 64 FP64 FMA/clk x 2 x sm_max_mhz"
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -122,6 +122,16 @@ mht_status mht_sync(mht_plan *plan);
 mht_status mht_stage_stats(const mht_plan *plan, int stage, int64_t *coef_bytes,
                            int32_t *n_mat, int32_t *n_tiles_fwd, int32_t *n_tiles_adj);
 
+/* Kernel-level profiling on the launching stream.  When on, every kernel
+ * launch of an apply is bracketed by CUDA events (kind 0 = forward stage,
+ * 1 = adjoint stage, 2 = adjoint group-sum).  mht_profile_get synchronises and
+ * returns the summed device time (ms) and launch count over all recorded
+ * launches of (kind, stage, nrhs); stage = -1 or nrhs = 0 match any.
+ * mht_profile_reset drops the records (keeps profiling on/off as is). */
+mht_status mht_set_profiling(mht_plan *plan, int on);
+mht_status mht_profile_get(mht_plan *plan, int kind, int stage, int nrhs, double *ms, int64_t *launches);
+mht_status mht_profile_reset(mht_plan *plan);
+
 /* Destroy the plan (synchronises its stream first).  NULL is a no-op. */
 void mht_plan_destroy(mht_plan *plan);
 

@@ -90,9 +90,9 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
 template <class S, int RB>
 __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Tile *__restrict__ tiles) {
   using X = Tr<S>;
-  const Tile tl = tiles[blockIdx.x];
+  const Tile tl = tiles[blockIdx.y];
   const DevBlock B = cx.blocks[tl.blk];
-  const int rhs0 = blockIdx.y * RB;
+  const int rhs0 = blockIdx.x * RB;  // RHS groups of one tile run back to back: T is shared in L2
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ra = tl.start + lane, rb = tl.start + 32 + lane;
   const bool va = lane < tl.count, vb = lane + 32 < tl.count;
@@ -185,9 +185,9 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Ti
                                                          int from_f) {
   using X = Tr<S>;
   constexpr int CPW = ADJ_COLS / (ADJ_THREADS / 32);  // columns per warp = 8
-  const Tile tl = tiles[blockIdx.x];
+  const Tile tl = tiles[blockIdx.y];
   const DevBlock B = cx.blocks[tl.blk];
-  const int rhs0 = blockIdx.y * RB;
+  const int rhs0 = blockIdx.x * RB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ S zs[ADJ_RCH][RB];
   S acc[CPW][RB];
@@ -275,23 +275,31 @@ __global__ void __launch_bounds__(256) reduce_kernel(const Ctx cx, const Piece *
   }
 }
 
+constexpr int MAX_GRID_Y = 65535;
+
 template <class S>
 void fwd_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, cudaStream_t st) {
-  if (cx.nrhs == 1) {
-    fwd_kernel<S, 1><<<dim3(ntiles, 1), FWD_THREADS, 0, st>>>(cx, tiles);
-  } else {
-    constexpr int RB = 4;
-    fwd_kernel<S, RB><<<dim3(ntiles, (cx.nrhs + RB - 1) / RB), FWD_THREADS, 0, st>>>(cx, tiles);
+  for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
+    const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
+    if (cx.nrhs == 1) {
+      fwd_kernel<S, 1><<<dim3(1, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
+    } else {
+      constexpr int RB = 4;
+      fwd_kernel<S, RB><<<dim3((cx.nrhs + RB - 1) / RB, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
+    }
   }
 }
 
 template <class S>
 void adj_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cudaStream_t st) {
-  if (cx.nrhs == 1) {
-    adj_kernel<S, 1><<<dim3(ntiles, 1), ADJ_THREADS, 0, st>>>(cx, tiles, from_f);
-  } else {
-    constexpr int RB = 2;
-    adj_kernel<S, RB><<<dim3(ntiles, (cx.nrhs + RB - 1) / RB), ADJ_THREADS, 0, st>>>(cx, tiles, from_f);
+  for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
+    const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
+    if (cx.nrhs == 1) {
+      adj_kernel<S, 1><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+    } else {
+      constexpr int RB = 2;
+      adj_kernel<S, RB><<<dim3((cx.nrhs + RB - 1) / RB, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+    }
   }
 }
 

@@ -89,8 +89,19 @@ struct mht_plan {
   void *d_hc = nullptr, *d_hf = nullptr;
   int host_nrhs = 0;
 
+  // profiling: one (start, stop) event pair per recorded launch
+  struct Rec {
+    int kind, stage, nrhs;
+    cudaEvent_t a, b;
+  };
+  bool prof = false;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+
   ~mht_plan() {
     if (stream) cudaStreamSynchronize(stream);
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd,
                     (void *)d_adj, (void *)d_pieces, (void *)d_rd, d_z, d_part, d_hc, d_hf})
       if (p) cudaFree(p);
@@ -582,12 +593,41 @@ Ctx make_ctx(mht_plan *P, int nrhs) {
   return cx;
 }
 
+cudaEvent_t next_event(mht_plan *P) {
+  if (P->ev_used == P->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    P->ev_pool.push_back(e);
+  }
+  return P->ev_pool[P->ev_used++];
+}
+
+// Launch wrapper: brackets the launch with events when profiling is on.
+template <class F>
+void timed(mht_plan *P, int kind, int stage, int nrhs, int count, F &&launch) {
+  if (count <= 0) return;
+  if (!P->prof) {
+    launch();
+    return;
+  }
+  cudaEvent_t a = next_event(P), b = next_event(P);
+  if (!a || !b) {
+    launch();
+    return;
+  }
+  cudaEventRecord(a, P->stream);
+  launch();
+  cudaEventRecord(b, P->stream);
+  P->recs.push_back({kind, stage, nrhs, a, b});
+}
+
 mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs) {
   Ctx cx = make_ctx(P, nrhs);
   cx.c = c;
   cx.fout = f;
   for (int s = 0; s < P->L + 2; ++s)
-    launch_fwd(P->cplx, cx, P->d_fwd + P->fwd[s].off, P->fwd[s].count, P->stream);
+    timed(P, 0, s, nrhs, P->fwd[s].count,
+          [&] { launch_fwd(P->cplx, cx, P->d_fwd + P->fwd[s].off, P->fwd[s].count, P->stream); });
   CUDA_TRY(cudaGetLastError());
   return MHT_OK;
 }
@@ -597,12 +637,18 @@ mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
   cx.fin = f;
   cx.cw = c;
   const int L = P->L;
-  launch_adj(P->cplx, cx, P->d_adj + P->adj[L + 1].off, P->adj[L + 1].count, true, P->stream);
+  timed(P, 1, L + 1, nrhs, P->adj[L + 1].count,
+        [&] { launch_adj(P->cplx, cx, P->d_adj + P->adj[L + 1].off, P->adj[L + 1].count, true, P->stream); });
   for (int s = L; s >= 0; --s) {
-    launch_reduce(P->cplx, cx, P->d_pieces + P->pieces[s].off, P->d_rd, P->pieces[s].count, P->stream);
-    launch_adj(P->cplx, cx, P->d_adj + P->adj[s].off, P->adj[s].count, false, P->stream);
+    timed(P, 2, s, nrhs, P->pieces[s].count, [&] {
+      launch_reduce(P->cplx, cx, P->d_pieces + P->pieces[s].off, P->d_rd, P->pieces[s].count, P->stream);
+    });
+    timed(P, 1, s, nrhs, P->adj[s].count,
+          [&] { launch_adj(P->cplx, cx, P->d_adj + P->adj[s].off, P->adj[s].count, false, P->stream); });
   }
-  launch_reduce(P->cplx, cx, P->d_pieces + P->cpieces.off, P->d_rd, P->cpieces.count, P->stream);
+  timed(P, 2, -1, nrhs, P->cpieces.count, [&] {
+    launch_reduce(P->cplx, cx, P->d_pieces + P->cpieces.off, P->d_rd, P->cpieces.count, P->stream);
+  });
   CUDA_TRY(cudaGetLastError());
   return MHT_OK;
 }
@@ -740,6 +786,39 @@ mht_status mht_stage_stats(const mht_plan *P, int stage, int64_t *coef_bytes, in
   if (n_mat) *n_mat = P->stage_nmat[stage];
   if (n_tiles_fwd) *n_tiles_fwd = P->fwd[stage].count;
   if (n_tiles_adj) *n_tiles_adj = P->adj[stage].count;
+  return MHT_OK;
+}
+
+mht_status mht_set_profiling(mht_plan *P, int on) {
+  if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
+  P->prof = on != 0;
+  return MHT_OK;
+}
+
+mht_status mht_profile_get(mht_plan *P, int kind, int stage, int nrhs, double *ms, int64_t *launches) {
+  if (!P || !ms || !launches) return fail(MHT_ERR_INVALID_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  double tot = 0;
+  int64_t cnt = 0;
+  for (const auto &r : P->recs) {
+    if (r.kind != kind || (stage >= 0 && r.stage != stage) || (nrhs > 0 && r.nrhs != nrhs)) continue;
+    float e = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&e, r.a, r.b));
+    tot += e;
+    ++cnt;
+  }
+  *ms = tot;
+  *launches = cnt;
+  return MHT_OK;
+}
+
+mht_status mht_profile_reset(mht_plan *P) {
+  if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
+  CUDA_TRY(cudaSetDevice(P->device));
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  P->recs.clear();
+  P->ev_used = 0;
   return MHT_OK;
 }
 

@@ -23,7 +23,8 @@ MHT_DTYPE_F64, MHT_DTYPE_C128 = 1, 2
 EXPORTED = [
     "mht_plan_load", "mht_plan_info_get", "mht_plan_set_stream", "mht_reserve", "mht_apply",
     "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host", "mht_set_graphs", "mht_sync",
-    "mht_stage_stats", "mht_plan_destroy", "mht_status_string", "mht_last_error", "mht_build_info",
+    "mht_stage_stats", "mht_set_profiling", "mht_profile_get", "mht_profile_reset", "mht_plan_destroy",
+    "mht_status_string", "mht_last_error", "mht_build_info",
 ]
 
 
@@ -61,6 +62,9 @@ def load_library(path: str = LIB_PATH):
     L.mht_sync.argtypes = [vp]
     L.mht_stage_stats.argtypes = [vp, i32, C.POINTER(i64), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                   C.POINTER(C.c_int32)]
+    L.mht_set_profiling.argtypes = [vp, i32]
+    L.mht_profile_get.argtypes = [vp, i32, i32, i32, C.POINTER(C.c_double), C.POINTER(i64)]
+    L.mht_profile_reset.argtypes = [vp]
     L.mht_plan_destroy.argtypes = [vp]
     L.mht_plan_destroy.restype = None
     L.mht_status_string.argtypes = [i32]
@@ -211,6 +215,18 @@ class Plan:
                    "mht_stage_stats")
             out.append(dict(stage=s, coef_bytes=cb.value, n_mat=nm.value, fwd_tiles=tf.value, adj_tiles=ta.value))
         return out
+
+    def set_profiling(self, on: bool):
+        _check(load_library().mht_set_profiling(self._h, int(bool(on))), "mht_set_profiling")
+
+    def profile_reset(self):
+        _check(load_library().mht_profile_reset(self._h), "mht_profile_reset")
+
+    def profile_get(self, kind: int, stage: int = -1, nrhs: int = 0):
+        """(total ms, launches) of recorded launches; kind 0 fwd, 1 adj, 2 group-sum."""
+        ms, n = C.c_double(), C.c_int64()
+        _check(load_library().mht_profile_get(self._h, kind, stage, nrhs, C.byref(ms), C.byref(n)), "mht_profile_get")
+        return ms.value, n.value
 
     def close(self):
         if getattr(self, "_h", None):

@@ -47,8 +47,26 @@ def setup(w: mi.Workload):
     return basis, perm, sp_off, fr_off
 
 
-def build_workload_plan(w: mi.Workload, path: str, workers=None, log=print, precompute_sphere=None):
+def build_workload_plan(w: mi.Workload, path: str, workers=None, log=print, precompute_sphere=None,
+                        builder: str = "cpu", device="cuda"):
+    """builder = "cpu" (numpy/scipy CPQR, multiprocess) or "gpu" (batched
+    torch CPQR on the device; same factorization, same file format)."""
     basis, perm, sp_off, fr_off = setup(w)
+    if builder == "gpu":
+        from .precompute import gpu_builder as G
+
+        if w.family == "flat":
+            tb = G.TorchFlatBasis(basis.x, basis.k, device)
+        elif w.family == "sphere":
+            tb = G.TorchTableBasis(G.sphere_table_torch(basis.theta, basis.phi, basis.lmax, device), np.float64)
+        else:
+            import torch
+
+            tb = G.TorchTableBasis(torch.as_tensor(np.asarray(basis.Phi), device=device), basis.dtype)
+        try:
+            return G.build_plan_gpu(tb, perm, sp_off, fr_off, w.L, w.tol, path, device=device, log=log)
+        finally:
+            del tb
     if isinstance(basis, SphereBasis) and (precompute_sphere or (precompute_sphere is None and w.n * w.m <= 6e9)):
         basis.precompute_all()
     return build_plan(basis, perm, sp_off, fr_off, w.L, w.tol, path, workers=workers, log=log)
@@ -62,12 +80,12 @@ def plan_cache_path(w: mi.Workload, root: str | None = None) -> str:
     return os.path.join(root, f"{tag}_{ex}.plan")
 
 
-def ensure_plan(w: mi.Workload, workers=None, log=print, root=None) -> str:
+def ensure_plan(w: mi.Workload, workers=None, log=print, root=None, builder="cpu", device="cuda") -> str:
     """Build the plan unless a complete file for this workload already exists
     (a cache only; a fresh box always rebuilds)."""
     p = plan_cache_path(w, root)
     if not os.path.exists(p):
-        build_workload_plan(w, p, workers=workers, log=log)
+        build_workload_plan(w, p, workers=workers, log=log, builder=builder, device=device)
     return p
 
 
