@@ -110,51 +110,52 @@ class ClockSampler:
 def dist_setup(args):
     import torch
 
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    lrank = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2605_21828_b200 import replicas
+
+    ws, rank, lrank = replicas.env_world()
+    gpu = torch.cuda.is_available()
+    if gpu:
+        torch.cuda.set_device(lrank)
     if ws > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(lrank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
-    else:
-        torch.cuda.set_device(0)
+        if gpu:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
+        else:
+            dist.init_process_group("gloo")
     return ws, rank, lrank
 
 
 def barrier(ws):
-    if ws > 1:
-        import torch.distributed as dist
+    from paper_2605_21828_b200 import replicas
 
-        dist.barrier()
+    replicas.barrier(ws)
 
 
 def allreduce_max(x, ws):
-    if ws == 1:
-        return x
     import torch
-    import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2605_21828_b200 import replicas
+
+    return replicas.allreduce_max(x, ws, device="cuda" if torch.cuda.is_available() else None)
 
 
 def get_plan(w, args, ws, rank, lrank):
     from paper_2605_21828_b200 import workloads as W
 
+    import torch
+
     path = W.plan_cache_path(w)
     if rank == 0 and not os.path.exists(path):
         t0 = time.time()
-        st = W.build_workload_plan(w, path + ".build", builder=args.builder, device=f"cuda:{lrank}",
+        builder = args.builder if torch.cuda.is_available() else "cpu"
+        st = W.build_workload_plan(w, path + ".build", builder=builder, device=f"cuda:{lrank}",
                                    log=lambda s: log(s))
         os.replace(path + ".build", path)
-        log(f"[bench] plan built in {time.time() - t0:.1f}s: {st['entries']} entries "
+        log(f"[bench] plan built ({builder}) in {time.time() - t0:.1f}s: {st['entries']} entries "
             f"({st['entries'] / st['dense_entries']:.3f} of dense), {st['plan_bytes'] / 1e9:.2f} GB")
-        import torch
-
-        torch.cuda.empty_cache()
+        if torch.cuda.is_available():
+            torch.cuda.empty_cache()
     barrier(ws)
     return path
 
@@ -223,16 +224,15 @@ def main():
 
     w = mi.WORKLOADS[args.workload]
     ws, rank, lrank = dist_setup(args)
-    if args.impl == "reference" and rank != 0:
-        # the reference arm runs on rank 0 only; other ranks exit without work
-        barrier(ws)
-        return
-    path = get_plan(w, args, 1 if args.impl == "reference" else ws, rank, lrank)
     if args.impl == "reference":
-        run_reference(args, w, path)
+        # the reference arm (the oracle on host cores) runs on rank 0 only;
+        # other ranks exit 0 without work
+        if rank == 0:
+            run_reference(args, w, get_plan(w, args, 1, rank, lrank))
         return
+    path = get_plan(w, args, ws, rank, lrank)
 
-    from paper_2605_21828_b200 import mht
+    from paper_2605_21828_b200 import mht, replicas
 
     P = mht.Plan(path, lrank)
     dev = torch.device("cuda", lrank)
@@ -243,8 +243,8 @@ def main():
     # inputs (each rank its own right-hand sides: replicas over RHS columns)
     ins, outs = {}, {}
     for r in widths:
-        c = mi.workload_coefficients(w, r + rank * 0) if rank == 0 else _rank_coef(w, r, rank)
-        y = mi.workload_adjoint_input(w, r) if rank == 0 else _rank_adj(w, r, rank)
+        c = replicas.rank_coefficients(w, r, rank)
+        y = replicas.rank_adjoint_inputs(w, r, rank)
         ins[("fwd", r)] = torch.from_numpy(c).to(dev)
         ins[("adj", r)] = torch.from_numpy(y).to(dev)
         outs[("fwd", r)] = torch.empty((r, w.n), dtype=P.torch_dtype, device=dev)
@@ -283,7 +283,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = allreduce_max(sum(step_ms), ws)
     transforms = sum(r for _, r in phases)
-    value = ws * transforms * args.steps / (total_ms / 1e3)
+    value = replicas.job_throughput(transforms * args.steps, ws, total_ms / 1e3)
 
     # ---- per-kernel live timing (events bracket every launch on its stream)
     stats = P.stage_stats()
@@ -353,18 +353,6 @@ def main():
         import torch.distributed as dist
 
         dist.destroy_process_group()
-
-
-def _rank_coef(w, r, rank):
-    if w.dtype == "complex128":
-        return mi.complex_gaussian(r, w.m, mi.SEED_COEF + 1000 * rank)
-    return mi.real_gaussian(r, w.m, mi.SEED_COEF + 1000 * rank)
-
-
-def _rank_adj(w, r, rank):
-    if w.dtype == "complex128":
-        return mi.complex_gaussian(r, w.n, mi.SEED_ADJ + 1000 * rank)
-    return mi.real_gaussian(r, w.n, mi.SEED_ADJ + 1000 * rank)
 
 
 def _e2e(P, phases, w, ws, args):

@@ -64,7 +64,7 @@ struct Ctx {  // per-launch pointers
   void *part;      // partial pool
   const void *fin; // f input (adjoint)
   void *fout;      // f output (forward)
-  int64_t m, n, Zt, Pt;
+  int64_t m, n, Zt, Pt;  // Zt/Pt: workspace entries per RHS (layout [entry][rhs])
   int nrhs;
 };
 
@@ -73,10 +73,15 @@ constexpr int FWD_THREADS = 128; // 4 warps split the columns
 constexpr int ADJ_COLS = 32;     // redundant columns per adjoint tile (8 per warp)
 constexpr int ADJ_THREADS = 128;
 constexpr int ADJ_RCH = 256;     // adjoint rows staged in smem per pass
+constexpr int MMA_COLS = 64;     // redundant columns per multi-RHS adjoint tile
 
 // Launchers (mht_kernels.cu).  is_complex selects double2 vs double.
 void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, void *stream);
 void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
+                void *stream);
+// multi-RHS (nrhs >= 2): DMMA kernels; forward uses the 64-row tiles, the
+// adjoint uses 64-column tiles (adjm lists).
+void launch_mma(bool is_complex, bool adjoint, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
                 void *stream);
 void launch_reduce(bool is_complex, const Ctx &ctx, const Piece *pieces, const int64_t *rd,
                    int npieces, void *stream);

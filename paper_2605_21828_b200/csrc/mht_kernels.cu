@@ -79,8 +79,8 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
   const bool s1 = q >= B.seg_len[0];  // no dynamic indexing: keeps B in registers
   const int64_t off = s1 ? B.seg_off[1] + (q - B.seg_len[0]) : B.seg_off[0] + q;
   const int32_t src = s1 ? B.seg_src[1] : B.seg_src[0];
-  if (src == SRC_C) return static_cast<const S *>(cx.c)[r * cx.m + off];
-  return static_cast<const S *>(cx.z)[r * cx.Zt + off];
+  if (src == SRC_C) return static_cast<const S *>(cx.c)[r * cx.m + off];  // user layout: column-major
+  return static_cast<const S *>(cx.z)[off * cx.nrhs + r];                   // workspace: RHS-fastest
 }
 
 // ------------------------------------------------------------------------
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Ti
       const int64_t j = cx.perm[B.out_off + row];
       static_cast<S *>(cx.fout)[r * cx.n + j] = s;
     } else {
-      static_cast<S *>(cx.z)[r * cx.Zt + B.out_off + row] = s;
+      static_cast<S *>(cx.z)[(B.out_off + row) * cx.nrhs + r] = s;
     }
   }
 }
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Ti
 template <class S>
 __device__ __forceinline__ S adj_in(const Ctx &cx, const DevBlock &B, int i, int r, bool from_f) {
   if (from_f) return static_cast<const S *>(cx.fin)[r * cx.n + cx.perm[B.out_off + i]];
-  return static_cast<const S *>(cx.z)[r * cx.Zt + B.out_off + i];
+  return static_cast<const S *>(cx.z)[(B.out_off + i) * cx.nrhs + r];
 }
 
 // ------------------------------------------------------------------------
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Ti
       const int q = (B.flags & F_RED_IOTA) ? col : cx.idx[B.red_off + col];
 #pragma unroll
       for (int k = 0; k < RB; ++k)
-        if (rhs0 + k < cx.nrhs) static_cast<S *>(cx.part)[(rhs0 + k) * cx.Pt + B.part_off + q] = acc[u][k];
+        if (rhs0 + k < cx.nrhs) static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0 + k] = acc[u][k];
     }
   }
   // skeleton part: w[skel[i]] = z[i]  (written once, by the block's first tile)
@@ -248,8 +248,225 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Ti
       const int i = e % B.n_skel, k = e / B.n_skel;
       if (rhs0 + k >= cx.nrhs) continue;
       const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
-      static_cast<S *>(cx.part)[(rhs0 + k) * cx.Pt + B.part_off + q] = adj_in<S>(cx, B, i, rhs0 + k, from_f);
+      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0 + k] = adj_in<S>(cx, B, i, rhs0 + k, from_f);
     }
+  }
+}
+
+// ------------------------------------------------------------------------
+// multi-RHS stages on the FP64 tensor pipe (DMMA, mma.sync m16n8k4 f64).
+//
+// Each block product is a dense contraction  OUT(M x N) = A(M x K) B(K x N):
+//   forward  A = T (r_out x n_red),        B = in[red] (n_red x nrhs)
+//   adjoint  A = T^* (n_red x r_out),      B = z       (r_out x nrhs)
+// A CTA owns a 64-row M tile (4 warps x 16 rows) and 8*NT right-hand sides;
+// K is streamed in chunks of 16 with a two-stage cp.async pipeline for the
+// factor tile (the HBM stream) and register-staged gathers for B.  Shared
+// memory holds both operands in mma-fragment order, so every fragment load is
+// one contiguous 512-byte LDS.128 per warp (no bank conflicts).  Complex
+// products are 4 real MMAs (re/im planes of the same fragments).
+// ------------------------------------------------------------------------
+constexpr int MM_BM = 64, MM_BK = 16, MM_THREADS = 128;
+
+__device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(b));
+}
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = valid ? BYTES : 0;  // src-size 0 -> zero fill
+  if (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <class S>
+struct Planes;  // re/im access for the MMA operands
+template <>
+struct Planes<double> {
+  static constexpr bool cplx = false;
+  static __device__ __forceinline__ double re(double v) { return v; }
+  static __device__ __forceinline__ double im(double) { return 0.0; }
+};
+template <>
+struct Planes<double2> {
+  static constexpr bool cplx = true;
+  static __device__ __forceinline__ double re(double2 v) { return v.x; }
+  static __device__ __forceinline__ double im(double2 v) { return v.y; }
+};
+
+template <class S, bool ADJ, int NT>
+__global__ void __launch_bounds__(MM_THREADS, 4) mma_kernel(const Ctx cx, const Tile *__restrict__ tiles, int from_f) {
+  using X = Tr<S>;
+  using PL = Planes<S>;
+  constexpr int NRT = 8 * NT;
+  constexpr int KS = MM_BK / 4;          // k4 steps per chunk
+  constexpr int AW = MM_BM / 16;         // warps along M
+  constexpr int B_PER_T = MM_BK * NRT / MM_THREADS;
+  // fragment-ordered operand buffers
+  __shared__ __align__(16) S As[2][KS][AW][2][32];
+  __shared__ __align__(16) S Bs[2][KS][NT][32];
+
+  const Tile tl = tiles[blockIdx.y];
+  const DevBlock B = cx.blocks[tl.blk];
+  const int rhs0 = blockIdx.x * NRT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
+  const int64_t ld = B.r_out;
+  const int K = ADJ ? B.r_out : B.n_red;
+  const int nchunks = (K + MM_BK - 1) / MM_BK;
+
+  // Operand staging.  Thread e writes fragment slot e (contiguous, conflict-free
+  // shared stores); slot e of a chunk is (k4, w, hi, gid, tig) with
+  // m = 16 w + 8 hi + gid and k = 4 k4 + tig, so a warp reads 4 (forward) or 8
+  // (adjoint) fully used 128/64-byte global segments.
+  S *As_flat = &As[0][0][0][0][0];
+  S *Bs_flat = &Bs[0][0][0][0];
+  auto load_A = [&](int kc, int buf) {
+    const int kb = kc * MM_BK;
+#pragma unroll
+    for (int i = 0; i < MM_BM * MM_BK / MM_THREADS; ++i) {
+      const int e = threadIdx.x + MM_THREADS * i;
+      const int tig_ = e & 3, gid_ = (e >> 2) & 7, hi = (e >> 5) & 1, w = (e >> 6) & (AW - 1), k4 = e >> 8;
+      const int m = w * 16 + hi * 8 + gid_, k = k4 * 4 + tig_;
+      const bool ok = m < tl.count && kb + k < K;
+      const S *src = ADJ ? T + (int64_t)(tl.start + m) * ld + (kb + k) : T + (int64_t)(kb + k) * ld + (tl.start + m);
+      cp_async<sizeof(S)>(As_flat + buf * (KS * AW * 2 * 32) + e, ok ? src : T, ok);
+    }
+  };
+  S breg[B_PER_T];
+  auto load_B = [&](int kc) {
+    const int kb = kc * MM_BK;
+#pragma unroll
+    for (int i = 0; i < B_PER_T; ++i) {
+      const int e = threadIdx.x + MM_THREADS * i;
+      const int tig_ = e & 3, gid_ = (e >> 2) & 7, t = (e >> 5) % NT, k4 = (e >> 5) / NT;
+      const int k = k4 * 4 + tig_, n = t * 8 + gid_;
+      const int r = rhs0 + n;
+      S v = X::zero();
+      if (kb + k < K && r < cx.nrhs) {
+        if (!ADJ) {
+          const int q = (B.flags & F_RED_IOTA) ? kb + k : cx.idx[B.red_off + kb + k];
+          v = in_value<S>(cx, B, q, r);
+        } else {
+          v = adj_in<S>(cx, B, kb + k, r, from_f != 0);
+        }
+      }
+      breg[i] = v;
+    }
+  };
+  auto store_B = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < B_PER_T; ++i) Bs_flat[buf * (KS * NT * 32) + threadIdx.x + MM_THREADS * i] = breg[i];
+  };
+
+  double cr[NT][4], ci[NT][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) cr[t][v] = ci[t][v] = 0.0;
+
+  if (nchunks > 0) {
+    load_A(0, 0);
+    cp_async_commit();
+    load_B(0);
+    store_B(0);
+    cp_async_wait_all();
+    __syncthreads();
+  }
+  for (int kc = 0; kc < nchunks; ++kc) {
+    const int cur = kc & 1, nxt = cur ^ 1;
+    const bool more = kc + 1 < nchunks;
+    if (more) {
+      load_A(kc + 1, nxt);
+      cp_async_commit();
+      load_B(kc + 1);
+    }
+#pragma unroll
+    for (int k4 = 0; k4 < KS; ++k4) {
+      const S a0 = As[cur][k4][warp][0][lane];
+      const S a1 = As[cur][k4][warp][1][lane];
+      const double ar0 = PL::re(a0), ar1 = PL::re(a1);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const S b = Bs[cur][k4][t][lane];
+        dmma(cr[t], ar0, ar1, PL::re(b));
+        if (PL::cplx) {
+          const double ai0 = PL::im(a0), ai1 = PL::im(a1);
+          if (!ADJ) {  // (Ar + i Ai)(Br + i Bi)
+            dmma(cr[t], -ai0, -ai1, PL::im(b));
+            dmma(ci[t], ar0, ar1, PL::im(b));
+            dmma(ci[t], ai0, ai1, PL::re(b));
+          } else {     // (Ar - i Ai)(Br + i Bi)
+            dmma(cr[t], ai0, ai1, PL::im(b));
+            dmma(ci[t], ar0, ar1, PL::im(b));
+            dmma(ci[t], -ai0, -ai1, PL::re(b));
+          }
+        }
+      }
+    }
+    if (more) store_B(nxt);
+    cp_async_wait_all();
+    __syncthreads();
+  }
+
+  // epilogue: C fragment (row gid / gid+8, cols 2 tig / 2 tig + 1)
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int m = warp * 16 + gid + 8 * (v >> 1);
+      const int r = rhs0 + t * 8 + 2 * tig + (v & 1);
+      if (m >= tl.count || r >= cx.nrhs) continue;
+      S val;
+      if constexpr (PL::cplx) {
+        val = make_double2(cr[t][v], ci[t][v]);
+      } else {
+        val = cr[t][v];
+      }
+      const int row = tl.start + m;
+      if (!ADJ) {
+        if (row < B.n_skel) {
+          const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
+          val = X::add(val, in_value<S>(cx, B, q, r));
+        }
+        if (B.flags & F_OUT_F)
+          static_cast<S *>(cx.fout)[r * cx.n + cx.perm[B.out_off + row]] = val;
+        else
+          static_cast<S *>(cx.z)[(B.out_off + row) * cx.nrhs + r] = val;
+      } else {
+        const int q = (B.flags & F_RED_IOTA) ? row : cx.idx[B.red_off + row];
+        static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = val;
+      }
+    }
+  }
+  if (ADJ && tl.start == 0 && B.n_skel > 0) {
+    for (int e = threadIdx.x; e < B.n_skel * NRT; e += MM_THREADS) {
+      const int i = e % B.n_skel, r = rhs0 + e / B.n_skel;
+      if (r >= cx.nrhs) continue;
+      const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
+      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = adj_in<S>(cx, B, i, r, from_f != 0);
+    }
+  }
+}
+
+template <class S, bool ADJ>
+void mma_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cudaStream_t st) {
+  for (int t0 = 0; t0 < ntiles; t0 += 65535) {
+    const int nt = ntiles - t0 < 65535 ? ntiles - t0 : 65535;
+    if (cx.nrhs >= 32)
+      mma_kernel<S, ADJ, 4><<<dim3((cx.nrhs + 31) / 32, nt), MM_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+    else if (cx.nrhs >= 16)
+      mma_kernel<S, ADJ, 2><<<dim3((cx.nrhs + 15) / 16, nt), MM_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+    else
+      mma_kernel<S, ADJ, 1><<<dim3((cx.nrhs + 7) / 8, nt), MM_THREADS, 0, st>>>(cx, tiles + t0, from_f);
   }
 }
 
@@ -263,15 +480,16 @@ __global__ void __launch_bounds__(256) reduce_kernel(const Ctx cx, const Piece *
   using X = Tr<S>;
   const Piece p = pieces[blockIdx.x];
   const S *part = static_cast<const S *>(cx.part);
-  for (int r = blockIdx.y; r < cx.nrhs; r += gridDim.y) {
-    for (int i = threadIdx.x; i < p.len; i += blockDim.x) {
-      S s = X::zero();
-      for (int q = 0; q < p.rd_count; ++q) s = X::add(s, part[r * cx.Pt + rd[p.rd_begin + q] + i]);
-      if (p.dst_src == SRC_C)
-        static_cast<S *>(cx.cw)[r * cx.m + p.dst_off + i] = s;
-      else
-        static_cast<S *>(cx.z)[r * cx.Zt + p.dst_off + i] = s;
-    }
+  const int nr = cx.nrhs;
+  const int total = p.len * nr;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int i = e / nr, r = e - (e / nr) * nr;  // RHS fastest (workspace layout)
+    S s = X::zero();
+    for (int q = 0; q < p.rd_count; ++q) s = X::add(s, part[(rd[p.rd_begin + q] + i) * nr + r]);
+    if (p.dst_src == SRC_C)
+      static_cast<S *>(cx.cw)[r * cx.m + p.dst_off + i] = s;
+    else
+      static_cast<S *>(cx.z)[(p.dst_off + i) * nr + r] = s;
   }
 }
 
@@ -281,12 +499,7 @@ template <class S>
 void fwd_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
     const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
-    if (cx.nrhs == 1) {
-      fwd_kernel<S, 1><<<dim3(1, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
-    } else {
-      constexpr int RB = 4;
-      fwd_kernel<S, RB><<<dim3((cx.nrhs + RB - 1) / RB, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
-    }
+    fwd_kernel<S, 1><<<dim3(1, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
   }
 }
 
@@ -294,12 +507,7 @@ template <class S>
 void adj_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
     const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
-    if (cx.nrhs == 1) {
-      adj_kernel<S, 1><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
-    } else {
-      constexpr int RB = 2;
-      adj_kernel<S, RB><<<dim3((cx.nrhs + RB - 1) / RB, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
-    }
+    adj_kernel<S, 1><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
   }
 }
 
@@ -322,14 +530,27 @@ void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, 
     adj_dispatch<double>(ctx, tiles, ntiles, in_from_f ? 1 : 0, (cudaStream_t)stream);
 }
 
+void launch_mma(bool is_complex, bool adjoint, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
+                void *stream) {
+  if (ntiles <= 0) return;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int ff = in_from_f ? 1 : 0;
+  if (is_complex) {
+    if (adjoint) mma_dispatch<double2, true>(ctx, tiles, ntiles, ff, st);
+    else mma_dispatch<double2, false>(ctx, tiles, ntiles, ff, st);
+  } else {
+    if (adjoint) mma_dispatch<double, true>(ctx, tiles, ntiles, ff, st);
+    else mma_dispatch<double, false>(ctx, tiles, ntiles, ff, st);
+  }
+}
+
 void launch_reduce(bool is_complex, const Ctx &ctx, const Piece *pieces, const int64_t *rd,
                    int npieces, void *stream) {
   if (npieces <= 0) return;
-  const int gy = ctx.nrhs < 8 ? ctx.nrhs : 8;
   if (is_complex)
-    reduce_kernel<double2><<<dim3(npieces, gy), 256, 0, (cudaStream_t)stream>>>(ctx, pieces, rd);
+    reduce_kernel<double2><<<npieces, 256, 0, (cudaStream_t)stream>>>(ctx, pieces, rd);
   else
-    reduce_kernel<double><<<dim3(npieces, gy), 256, 0, (cudaStream_t)stream>>>(ctx, pieces, rd);
+    reduce_kernel<double><<<npieces, 256, 0, (cudaStream_t)stream>>>(ctx, pieces, rd);
 }
 
 }  // namespace mht

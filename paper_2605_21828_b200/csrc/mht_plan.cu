@@ -75,10 +75,11 @@ struct mht_plan {
   DevBlock *d_blocks = nullptr;
   Tile *d_fwd = nullptr;
   Tile *d_adj = nullptr;
+  Tile *d_adjm = nullptr;
   Piece *d_pieces = nullptr;
   int64_t *d_rd = nullptr;
 
-  std::vector<Range> fwd, adj, pieces;  // per stage 0..L+1
+  std::vector<Range> fwd, adj, adjm, pieces;  // per stage 0..L+1
   Range cpieces;
   std::vector<int64_t> stage_coef_bytes;
   std::vector<int32_t> stage_nmat;
@@ -103,7 +104,7 @@ struct mht_plan {
     if (stream) cudaStreamSynchronize(stream);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd,
-                    (void *)d_adj, (void *)d_pieces, (void *)d_rd, d_z, d_part, d_hc, d_hf})
+                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, d_z, d_part, d_hc, d_hf})
       if (p) cudaFree(p);
   }
 };
@@ -420,13 +421,21 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
   P->n_mat = (int)blocks.size();
 
   // ------------------------------------------------ tiles (LPT order per stage)
-  std::vector<std::vector<std::pair<int64_t, Tile>>> ft(L + 2), at(L + 2);
+  std::vector<std::vector<std::pair<int64_t, Tile>>> ft(L + 2), at(L + 2), amt(L + 2);
   for (int i = 0; i < (int)blocks.size(); ++i) {
     const DevBlock &D = blocks[i];
     const int s = block_stage[i];
     for (int r0 = 0; r0 < D.r_out; r0 += FWD_ROWS) {
       int cnt = std::min(FWD_ROWS, D.r_out - r0);
       ft[s].push_back({(int64_t)cnt * (D.n_red + 4), Tile{i, r0, cnt, 0}});
+    }
+    if (D.n_red == 0) {
+      amt[s].push_back({(int64_t)D.r_out + D.n_skel, Tile{i, 0, 0, 0}});
+    } else {
+      for (int c0 = 0; c0 < D.n_red; c0 += MMA_COLS) {
+        int cnt = std::min(MMA_COLS, D.n_red - c0);
+        amt[s].push_back({(int64_t)cnt * (D.r_out + 4) + (c0 == 0 ? D.n_skel : 0), Tile{i, c0, cnt, 0}});
+      }
     }
     if (D.n_red == 0) {
       at[s].push_back({(int64_t)D.r_out + D.n_skel, Tile{i, 0, 0, 0}});
@@ -437,9 +446,10 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
       }
     }
   }
-  std::vector<Tile> fwd_all, adj_all;
+  std::vector<Tile> fwd_all, adj_all, adjm_all;
   P->fwd.assign(L + 2, Range{});
   P->adj.assign(L + 2, Range{});
+  P->adjm.assign(L + 2, Range{});
   auto by_cost = [](const std::pair<int64_t, Tile> &a, const std::pair<int64_t, Tile> &b) {
     return a.first > b.first;
   };
@@ -450,6 +460,9 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
     for (auto &x : ft[s]) fwd_all.push_back(x.second);
     P->adj[s] = Range{(int32_t)adj_all.size(), (int32_t)at[s].size()};
     for (auto &x : at[s]) adj_all.push_back(x.second);
+    std::stable_sort(amt[s].begin(), amt[s].end(), by_cost);
+    P->adjm[s] = Range{(int32_t)adjm_all.size(), (int32_t)amt[s].size()};
+    for (auto &x : amt[s]) adjm_all.push_back(x.second);
   }
 
   // ------------------------------------------------ adjoint group-sum pieces
@@ -558,6 +571,7 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
   if ((st = upload(&P->d_blocks, blocks, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_fwd, fwd_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_adj, adj_all, P->device_bytes)) != MHT_OK) return st;
+  if ((st = upload(&P->d_adjm, adjm_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_pieces, pieces_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_rd, rd_all, P->device_bytes)) != MHT_OK) return st;
   return MHT_OK;
@@ -626,8 +640,12 @@ mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs) {
   cx.c = c;
   cx.fout = f;
   for (int s = 0; s < P->L + 2; ++s)
-    timed(P, 0, s, nrhs, P->fwd[s].count,
-          [&] { launch_fwd(P->cplx, cx, P->d_fwd + P->fwd[s].off, P->fwd[s].count, P->stream); });
+    timed(P, 0, s, nrhs, P->fwd[s].count, [&] {
+      if (nrhs == 1)
+        launch_fwd(P->cplx, cx, P->d_fwd + P->fwd[s].off, P->fwd[s].count, P->stream);
+      else
+        launch_mma(P->cplx, false, cx, P->d_fwd + P->fwd[s].off, P->fwd[s].count, false, P->stream);
+    });
   CUDA_TRY(cudaGetLastError());
   return MHT_OK;
 }
@@ -637,14 +655,21 @@ mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
   cx.fin = f;
   cx.cw = c;
   const int L = P->L;
-  timed(P, 1, L + 1, nrhs, P->adj[L + 1].count,
-        [&] { launch_adj(P->cplx, cx, P->d_adj + P->adj[L + 1].off, P->adj[L + 1].count, true, P->stream); });
+  auto adj_stage = [&](int s, bool from_f) {
+    if (nrhs == 1)
+      timed(P, 1, s, nrhs, P->adj[s].count,
+            [&] { launch_adj(P->cplx, cx, P->d_adj + P->adj[s].off, P->adj[s].count, from_f, P->stream); });
+    else
+      timed(P, 1, s, nrhs, P->adjm[s].count, [&] {
+        launch_mma(P->cplx, true, cx, P->d_adjm + P->adjm[s].off, P->adjm[s].count, from_f, P->stream);
+      });
+  };
+  adj_stage(L + 1, true);
   for (int s = L; s >= 0; --s) {
     timed(P, 2, s, nrhs, P->pieces[s].count, [&] {
       launch_reduce(P->cplx, cx, P->d_pieces + P->pieces[s].off, P->d_rd, P->pieces[s].count, P->stream);
     });
-    timed(P, 1, s, nrhs, P->adj[s].count,
-          [&] { launch_adj(P->cplx, cx, P->d_adj + P->adj[s].off, P->adj[s].count, false, P->stream); });
+    adj_stage(s, false);
   }
   timed(P, 2, -1, nrhs, P->cpieces.count, [&] {
     launch_reduce(P->cplx, cx, P->d_pieces + P->cpieces.off, P->d_rd, P->cpieces.count, P->stream);

@@ -89,7 +89,7 @@ def flat_dense(oracle_lib, w):
 
 def test_flat_small_parity(gpu, oracle_lib, plans):
     path, w = flat_case(plans, 2048, 32, 4, 1e-8)
-    check_plan(gpu, oracle_lib, path, w, (1, 2, 3, 5, 8, 32), dense=flat_dense(oracle_lib, w))
+    check_plan(gpu, oracle_lib, path, w, (1, 2, 3, 5, 8, 16, 17, 32, 40), dense=flat_dense(oracle_lib, w))
 
 
 def test_flat_loose_tolerance_compressed(gpu, oracle_lib, plans):
@@ -113,7 +113,7 @@ def test_sphere_parity(gpu, oracle_lib, plans):
     W.build_workload_plan(w, path, workers=8, log=None)
     th, ph, _ = mi.sphere_points(w.n)
     dense = lambda c, y: (oracle_lib.sphere_synth(th, ph, lmax, c), oracle_lib.sphere_analysis(th, ph, lmax, y))
-    check_plan(gpu, oracle_lib, path, w, (1, 3, 32), dense=dense)
+    check_plan(gpu, oracle_lib, path, w, (1, 3, 16, 33, 64), dense=dense)
 
 
 def test_ragged_leaves_and_L0(gpu, oracle_lib, plans):
