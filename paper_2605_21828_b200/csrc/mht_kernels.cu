@@ -13,6 +13,9 @@
 // registers.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "mht_internal.cuh"
 
 namespace mht {
@@ -285,6 +288,8 @@ __device__ __forceinline__ void cp_async(void *smem, const void *gmem, bool vali
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <class S>
 struct Planes;  // re/im access for the MMA operands
@@ -301,17 +306,27 @@ struct Planes<double2> {
   static __device__ __forceinline__ double im(double2 v) { return v.y; }
 };
 
-template <class S, bool ADJ, int NT>
-__global__ void __launch_bounds__(MM_THREADS, 4) mma_kernel(const Ctx cx, const Tile *__restrict__ tiles, int from_f) {
+// M3: complex products by Gauss's 3-multiplication form (P1 = Ar Br, P2 = Ai Bi,
+// P3 = (Ar + Ai)(Br + Bi); re = P1 - P2, im = P3 - P1 - P2) — 3 DMMAs instead of 4.
+// MINB: CTAs per SM the register budget is sized for.
+template <class S, bool ADJ, int NT, bool M3, int MINB>
+__global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, const Tile *__restrict__ tiles, int from_f) {
   using X = Tr<S>;
   using PL = Planes<S>;
+  constexpr bool CPLX = PL::cplx;
+  constexpr bool G3 = CPLX && M3;
   constexpr int NRT = 8 * NT;
   constexpr int KS = MM_BK / 4;          // k4 steps per chunk
   constexpr int AW = MM_BM / 16;         // warps along M
   constexpr int B_PER_T = MM_BK * NRT / MM_THREADS;
-  // fragment-ordered operand buffers
-  __shared__ __align__(16) S As[2][KS][AW][2][32];
-  __shared__ __align__(16) S Bs[2][KS][NT][32];
+  constexpr int A_CH = KS * AW * 2 * 32; // scalars per A chunk (fragment order [k4][w][hi][lane])
+  constexpr int B_CH = KS * NT * 32;     // scalars per B chunk ([k4][t][lane])
+  // two-stage ring of fragment-ordered operand buffers.  Static shared
+  // memory measured faster than a dynamic 2/3-stage ring (the default carveout
+  // keeps more L1 for the B gathers; profiles/r01_mma_variants.txt).
+  constexpr int NB = 2;
+  __shared__ __align__(16) S As[NB * A_CH];
+  __shared__ __align__(16) S Bs[NB * B_CH];
 
   const Tile tl = tiles[blockIdx.y];
   const DevBlock B = cx.blocks[tl.blk];
@@ -322,15 +337,15 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_kernel(const Ctx cx, const 
   const int64_t ld = B.r_out;
   const int K = ADJ ? B.r_out : B.n_red;
   const int nchunks = (K + MM_BK - 1) / MM_BK;
+  const bool red_iota = (B.flags & F_RED_IOTA) != 0;
 
   // Operand staging.  Thread e writes fragment slot e (contiguous, conflict-free
   // shared stores); slot e of a chunk is (k4, w, hi, gid, tig) with
   // m = 16 w + 8 hi + gid and k = 4 k4 + tig, so a warp reads 4 (forward) or 8
   // (adjoint) fully used 128/64-byte global segments.
-  S *As_flat = &As[0][0][0][0][0];
-  S *Bs_flat = &Bs[0][0][0][0];
-  auto load_A = [&](int kc, int buf) {
+  auto load_A = [&](int kc) {
     const int kb = kc * MM_BK;
+    S *dst = As + (kc % NB) * A_CH;
 #pragma unroll
     for (int i = 0; i < MM_BM * MM_BK / MM_THREADS; ++i) {
       const int e = threadIdx.x + MM_THREADS * i;
@@ -338,7 +353,20 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_kernel(const Ctx cx, const 
       const int m = w * 16 + hi * 8 + gid_, k = k4 * 4 + tig_;
       const bool ok = m < tl.count && kb + k < K;
       const S *src = ADJ ? T + (int64_t)(tl.start + m) * ld + (kb + k) : T + (int64_t)(kb + k) * ld + (tl.start + m);
-      cp_async<sizeof(S)>(As_flat + buf * (KS * AW * 2 * 32) + e, ok ? src : T, ok);
+      cp_async<sizeof(S)>(dst + e, ok ? src : T, ok);
+    }
+  };
+  // B gather: the forward's redundant-position indices are fetched one chunk
+  // ahead (qreg), so the value loads never wait on an index load.
+  int qreg[B_PER_T];
+  auto load_q = [&](int kc) {
+    if (ADJ) return;
+    const int kb = kc * MM_BK;
+#pragma unroll
+    for (int i = 0; i < B_PER_T; ++i) {
+      const int e = threadIdx.x + MM_THREADS * i;
+      const int k = ((e >> 5) / NT) * 4 + (e & 3);
+      qreg[i] = (kb + k < K) ? (red_iota ? kb + k : __ldg(cx.idx + B.red_off + kb + k)) : 0;
     }
   };
   S breg[B_PER_T];
@@ -351,72 +379,77 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_kernel(const Ctx cx, const 
       const int k = k4 * 4 + tig_, n = t * 8 + gid_;
       const int r = rhs0 + n;
       S v = X::zero();
-      if (kb + k < K && r < cx.nrhs) {
-        if (!ADJ) {
-          const int q = (B.flags & F_RED_IOTA) ? kb + k : cx.idx[B.red_off + kb + k];
-          v = in_value<S>(cx, B, q, r);
-        } else {
-          v = adj_in<S>(cx, B, kb + k, r, from_f != 0);
-        }
-      }
+      if (kb + k < K && r < cx.nrhs) v = ADJ ? adj_in<S>(cx, B, kb + k, r, from_f != 0) : in_value<S>(cx, B, qreg[i], r);
       breg[i] = v;
     }
   };
-  auto store_B = [&](int buf) {
+  auto store_B = [&](int kc) {
+    S *dst = Bs + (kc % NB) * B_CH;
 #pragma unroll
-    for (int i = 0; i < B_PER_T; ++i) Bs_flat[buf * (KS * NT * 32) + threadIdx.x + MM_THREADS * i] = breg[i];
+    for (int i = 0; i < B_PER_T; ++i) dst[threadIdx.x + MM_THREADS * i] = breg[i];
   };
 
-  double cr[NT][4], ci[NT][4];
+  // accumulators: 4M uses (re, im); 3M uses (P1, P2, P3)
+  double c0[NT][4], c1[NT][4], c2[G3 ? NT : 1][4];
 #pragma unroll
   for (int t = 0; t < NT; ++t)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) cr[t][v] = ci[t][v] = 0.0;
+    for (int v = 0; v < 4; ++v) c0[t][v] = c1[t][v] = 0.0;
+#pragma unroll
+  for (int t = 0; t < (G3 ? NT : 1); ++t)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) c2[t][v] = 0.0;
 
+  // two-stage ring, sync at the bottom of the iteration
   if (nchunks > 0) {
-    load_A(0, 0);
+    load_A(0);
     cp_async_commit();
+    load_q(0);
     load_B(0);
     store_B(0);
-    cp_async_wait_all();
+    if (nchunks > 1) load_q(1);
+    cp_async_wait<0>();
     __syncthreads();
   }
   for (int kc = 0; kc < nchunks; ++kc) {
-    const int cur = kc & 1, nxt = cur ^ 1;
     const bool more = kc + 1 < nchunks;
     if (more) {
-      load_A(kc + 1, nxt);
+      load_A(kc + 1);
       cp_async_commit();
       load_B(kc + 1);
+      if (kc + 2 < nchunks) load_q(kc + 2);
     }
+    const S *Ac = As + (kc % NB) * A_CH;
+    const S *Bc = Bs + (kc % NB) * B_CH;
 #pragma unroll
     for (int k4 = 0; k4 < KS; ++k4) {
-      const S a0 = As[cur][k4][warp][0][lane];
-      const S a1 = As[cur][k4][warp][1][lane];
+      const S a0 = Ac[((k4 * AW + warp) * 2 + 0) * 32 + lane];
+      const S a1 = Ac[((k4 * AW + warp) * 2 + 1) * 32 + lane];
       const double ar0 = PL::re(a0), ar1 = PL::re(a1);
+      // conj(T) for the adjoint
+      const double ai0 = ADJ ? -PL::im(a0) : PL::im(a0), ai1 = ADJ ? -PL::im(a1) : PL::im(a1);
+      const double as0 = ar0 + ai0, as1 = ar1 + ai1;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        const S b = Bs[cur][k4][t][lane];
-        dmma(cr[t], ar0, ar1, PL::re(b));
-        if (PL::cplx) {
-          const double ai0 = PL::im(a0), ai1 = PL::im(a1);
-          if (!ADJ) {  // (Ar + i Ai)(Br + i Bi)
-            dmma(cr[t], -ai0, -ai1, PL::im(b));
-            dmma(ci[t], ar0, ar1, PL::im(b));
-            dmma(ci[t], ai0, ai1, PL::re(b));
-          } else {     // (Ar - i Ai)(Br + i Bi)
-            dmma(cr[t], ai0, ai1, PL::im(b));
-            dmma(ci[t], ar0, ar1, PL::im(b));
-            dmma(ci[t], -ai0, -ai1, PL::re(b));
-          }
+        const S b = Bc[(k4 * NT + t) * 32 + lane];
+        if constexpr (!CPLX) {
+          dmma(c0[t], ar0, ar1, PL::re(b));
+        } else if constexpr (G3) {
+          dmma(c0[t], ar0, ar1, PL::re(b));
+          dmma(c1[t], ai0, ai1, PL::im(b));
+          dmma(c2[t], as0, as1, PL::re(b) + PL::im(b));
+        } else {  // (Ar + i Ai)(Br + i Bi)
+          dmma(c0[t], ar0, ar1, PL::re(b));
+          dmma(c0[t], -ai0, -ai1, PL::im(b));
+          dmma(c1[t], ar0, ar1, PL::im(b));
+          dmma(c1[t], ai0, ai1, PL::re(b));
         }
       }
     }
-    if (more) store_B(nxt);
-    cp_async_wait_all();
+    if (more) store_B(kc + 1);
+    cp_async_wait<0>();
     __syncthreads();
   }
-
   // epilogue: C fragment (row gid / gid+8, cols 2 tig / 2 tig + 1)
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
@@ -426,10 +459,12 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_kernel(const Ctx cx, const 
       const int r = rhs0 + t * 8 + 2 * tig + (v & 1);
       if (m >= tl.count || r >= cx.nrhs) continue;
       S val;
-      if constexpr (PL::cplx) {
-        val = make_double2(cr[t][v], ci[t][v]);
+      if constexpr (!CPLX) {
+        val = c0[t][v];
+      } else if constexpr (G3) {
+        val = make_double2(c0[t][v] - c1[t][v], c2[t][v] - c0[t][v] - c1[t][v]);
       } else {
-        val = cr[t][v];
+        val = make_double2(c0[t][v], c1[t][v]);
       }
       const int row = tl.start + m;
       if (!ADJ) {
@@ -442,7 +477,7 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_kernel(const Ctx cx, const 
         else
           static_cast<S *>(cx.z)[(B.out_off + row) * cx.nrhs + r] = val;
       } else {
-        const int q = (B.flags & F_RED_IOTA) ? row : cx.idx[B.red_off + row];
+        const int q = red_iota ? row : cx.idx[B.red_off + row];
         static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = val;
       }
     }
@@ -457,16 +492,42 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_kernel(const Ctx cx, const 
   }
 }
 
+// Multi-RHS configuration (compile-time variants; default picked from the
+// measurements in profiles/, override with MHT_MMA=4m|3m for experiments).
+inline int mma_variant() {
+  static int v = [] {
+    const char *e = getenv("MHT_MMA");
+    if (e && !strcmp(e, "4m")) return 0;   // 4 real MMAs per complex product, 32 RHS per CTA
+    if (e && !strcmp(e, "3m")) return 1;   // 3M, 32 RHS per CTA (3 CTAs/SM)
+    return 1;
+  }();
+  return v;
+}
+
+template <class S, bool ADJ, int NT, bool M3, int MINB>
+void mma_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
+  mma_kernel<S, ADJ, NT, M3, MINB><<<dim3((cx.nrhs + 8 * NT - 1) / (8 * NT), nt), MM_THREADS, 0, st>>>(cx, tiles, from_f);
+}
+
+template <class S, bool ADJ, bool M3, int MINB, int NTMAX>
+void mma_launch_nt(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
+  if (NTMAX >= 4 && cx.nrhs >= 32)
+    mma_launch<S, ADJ, 4, M3, MINB>(cx, tiles, nt, from_f, st);
+  else if (cx.nrhs >= 16)
+    mma_launch<S, ADJ, 2, M3, 4>(cx, tiles, nt, from_f, st);
+  else
+    mma_launch<S, ADJ, 1, M3, 4>(cx, tiles, nt, from_f, st);
+}
+
 template <class S, bool ADJ>
 void mma_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += 65535) {
     const int nt = ntiles - t0 < 65535 ? ntiles - t0 : 65535;
-    if (cx.nrhs >= 32)
-      mma_kernel<S, ADJ, 4><<<dim3((cx.nrhs + 31) / 32, nt), MM_THREADS, 0, st>>>(cx, tiles + t0, from_f);
-    else if (cx.nrhs >= 16)
-      mma_kernel<S, ADJ, 2><<<dim3((cx.nrhs + 15) / 16, nt), MM_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+    const int v = Planes<S>::cplx ? mma_variant() : 0;
+    if (v >= 1)
+      mma_launch_nt<S, ADJ, true, 3, 4>(cx, tiles + t0, nt, from_f, st);
     else
-      mma_kernel<S, ADJ, 1><<<dim3((cx.nrhs + 7) / 8, nt), MM_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+      mma_launch_nt<S, ADJ, false, 4, 4>(cx, tiles + t0, nt, from_f, st);
   }
 }
 
