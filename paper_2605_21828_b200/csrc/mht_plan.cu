@@ -68,6 +68,25 @@ struct mht_plan {
   int64_t plan_bytes = 0, factor_entries = 0, index_entries = 0, device_bytes = 0;
   int n_mat = 0, n_alias = 0;
   bool graphs = true;
+  // CUDA-graph cache: one executable graph per (direction, nrhs, src, dst),
+  // captured on an internal stream and launched on the caller's stream.
+  struct GraphKey {
+    int dir, nrhs;
+    const void *src;
+    void *dst;
+    bool operator<(const GraphKey &o) const {
+      if (dir != o.dir) return dir < o.dir;
+      if (nrhs != o.nrhs) return nrhs < o.nrhs;
+      if (src != o.src) return src < o.src;
+      return dst < o.dst;
+    }
+  };
+  std::map<GraphKey, cudaGraphExec_t> gcache;
+  cudaStream_t cap_stream = nullptr;
+  void clear_graphs() {
+    for (auto &kv : gcache) cudaGraphExecDestroy(kv.second);
+    gcache.clear();
+  }
 
   void *d_coef = nullptr;
   int32_t *d_idx = nullptr;
@@ -102,6 +121,8 @@ struct mht_plan {
 
   ~mht_plan() {
     if (stream) cudaStreamSynchronize(stream);
+    clear_graphs();
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd,
                     (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, d_z, d_part, d_hc, d_hf})
@@ -580,6 +601,7 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
 mht_status ensure_ws(mht_plan *P, int nrhs) {
   if (nrhs <= P->ws_nrhs) return MHT_OK;
   CUDA_TRY(cudaStreamSynchronize(P->stream));
+  P->clear_graphs();
   if (P->d_z) cudaFree(P->d_z);
   if (P->d_part) cudaFree(P->d_part);
   P->d_z = P->d_part = nullptr;
@@ -678,6 +700,40 @@ mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
   return MHT_OK;
 }
 
+// Replay (or capture, then replay) the whole stage sequence of one apply as a
+// CUDA graph.  Profiling bypasses graphs (per-launch events).
+mht_status run_dir(mht_plan *P, int dir, const void *src, void *dst, int nrhs) {
+  if (!P->graphs || P->prof) return dir == 0 ? run_forward(P, src, dst, nrhs) : run_adjoint(P, src, dst, nrhs);
+  mht_plan::GraphKey key{dir, nrhs, src, dst};
+  auto it = P->gcache.find(key);
+  if (it == P->gcache.end()) {
+    if (!P->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&P->cap_stream, cudaStreamNonBlocking));
+    if (P->gcache.size() >= 32) P->clear_graphs();
+    cudaStream_t user = P->stream;
+    P->stream = P->cap_stream;
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal);
+    mht_status st = MHT_OK;
+    if (e == cudaSuccess) {
+      st = dir == 0 ? run_forward(P, src, dst, nrhs) : run_adjoint(P, src, dst, nrhs);
+      e = cudaStreamEndCapture(P->cap_stream, &g);
+    }
+    P->stream = user;
+    if (st != MHT_OK) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (e != cudaSuccess) return fail(MHT_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(MHT_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    it = P->gcache.emplace(key, ex).first;
+  }
+  CUDA_TRY(cudaGraphLaunch(it->second, P->stream));
+  return MHT_OK;
+}
+
 }  // namespace
 
 // ====================================================================== ABI
@@ -742,7 +798,7 @@ mht_status mht_apply(mht_plan *P, const void *c, void *f, int nrhs) {
   CUDA_TRY(cudaSetDevice(P->device));
   mht_status s = ensure_ws(P, nrhs);
   if (s != MHT_OK) return s;
-  return run_forward(P, c, f, nrhs);
+  return run_dir(P, 0, c, f, nrhs);
 }
 
 mht_status mht_apply_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
@@ -750,12 +806,13 @@ mht_status mht_apply_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
   CUDA_TRY(cudaSetDevice(P->device));
   mht_status s = ensure_ws(P, nrhs);
   if (s != MHT_OK) return s;
-  return run_adjoint(P, f, c, nrhs);
+  return run_dir(P, 1, f, c, nrhs);
 }
 
 static mht_status ensure_host_staging(mht_plan *P, int nrhs) {
   if (nrhs <= P->host_nrhs) return MHT_OK;
   CUDA_TRY(cudaStreamSynchronize(P->stream));
+  P->clear_graphs();
   if (P->d_hc) cudaFree(P->d_hc);
   if (P->d_hf) cudaFree(P->d_hf);
   P->d_hc = P->d_hf = nullptr;
@@ -772,7 +829,7 @@ mht_status mht_apply_host(mht_plan *P, const void *c_host, void *f_host, int nrh
   mht_status s;
   if ((s = ensure_ws(P, nrhs)) != MHT_OK || (s = ensure_host_staging(P, nrhs)) != MHT_OK) return s;
   CUDA_TRY(cudaMemcpyAsync(P->d_hc, c_host, (size_t)P->m * nrhs * P->ssz, cudaMemcpyHostToDevice, P->stream));
-  if ((s = run_forward(P, P->d_hc, P->d_hf, nrhs)) != MHT_OK) return s;
+  if ((s = run_dir(P, 0, P->d_hc, P->d_hf, nrhs)) != MHT_OK) return s;
   CUDA_TRY(cudaMemcpyAsync(f_host, P->d_hf, (size_t)P->n * nrhs * P->ssz, cudaMemcpyDeviceToHost, P->stream));
   CUDA_TRY(cudaStreamSynchronize(P->stream));
   return MHT_OK;
@@ -784,7 +841,7 @@ mht_status mht_apply_adjoint_host(mht_plan *P, const void *f_host, void *c_host,
   mht_status s;
   if ((s = ensure_ws(P, nrhs)) != MHT_OK || (s = ensure_host_staging(P, nrhs)) != MHT_OK) return s;
   CUDA_TRY(cudaMemcpyAsync(P->d_hf, f_host, (size_t)P->n * nrhs * P->ssz, cudaMemcpyHostToDevice, P->stream));
-  if ((s = run_adjoint(P, P->d_hf, P->d_hc, nrhs)) != MHT_OK) return s;
+  if ((s = run_dir(P, 1, P->d_hf, P->d_hc, nrhs)) != MHT_OK) return s;
   CUDA_TRY(cudaMemcpyAsync(c_host, P->d_hc, (size_t)P->m * nrhs * P->ssz, cudaMemcpyDeviceToHost, P->stream));
   CUDA_TRY(cudaStreamSynchronize(P->stream));
   return MHT_OK;
@@ -793,6 +850,7 @@ mht_status mht_apply_adjoint_host(mht_plan *P, const void *f_host, void *c_host,
 mht_status mht_set_graphs(mht_plan *P, int on) {
   if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
   P->graphs = on != 0;
+  if (!P->graphs) P->clear_graphs();
   return MHT_OK;
 }
 

@@ -90,7 +90,8 @@ def sphere_table_torch(theta, phi, lmax, device, chunk=4096):
     ms = np.arange(M) - ls * ls - ls
     am = torch.as_tensor(np.abs(ms), device=device)
     lt = torch.as_tensor(ls, device=device)
-    scale = torch.where(torch.as_tensor(ms, device=device) == 0, 1.0, math.sqrt(2.0)).to(torch.float64)
+    # float64 from numpy: torch.where on two Python scalars would produce float32 (sqrt 2 to 1e-8)
+    scale = torch.as_tensor(np.where(ms == 0, 1.0, math.sqrt(2.0)).astype(np.float64), device=device)
     pos = torch.as_tensor(ms >= 0, device=device)
     mvec = torch.arange(lmax + 1, dtype=torch.float64, device=device)
     for s in range(0, n, chunk):

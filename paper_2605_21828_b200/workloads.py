@@ -72,12 +72,16 @@ def build_workload_plan(w: mi.Workload, path: str, workers=None, log=print, prec
     return build_plan(basis, perm, sp_off, fr_off, w.L, w.tol, path, workers=workers, log=log)
 
 
+# bump when the builders' numerics change so cached plans are never reused across versions
+BUILDER_VERSION = 2
+
+
 def plan_cache_path(w: mi.Workload, root: str | None = None) -> str:
     root = root or os.environ.get("MHT_PLAN_DIR") or ("/dev/shm/mht_plans" if os.path.isdir("/dev/shm") else "/tmp/mht_plans")
     os.makedirs(root, exist_ok=True)
     tag = f"{w.name}_{w.family}_n{w.n}_m{w.m}_L{w.L}_tol{w.tol:g}"
     ex = "_".join(f"{k}{v}" for k, v in sorted(w.extra.items()))
-    return os.path.join(root, f"{tag}_{ex}.plan")
+    return os.path.join(root, f"{tag}_{ex}_b{BUILDER_VERSION}.plan")
 
 
 def ensure_plan(w: mi.Workload, workers=None, log=print, root=None, builder="cpu", device="cuda") -> str:
