@@ -33,14 +33,16 @@ struct DevBlock {
   int32_t seg_len[2];
   int32_t seg_src[2];  // SRC_C | SRC_Z
   int32_t r_out, r_in, n_skel, n_red;
-  int32_t flags, pad;
+  int32_t flags;
+  int32_t pad;  // forward column splits (nrhs = 1), 0 = none
 };
 static_assert(sizeof(DevBlock) == 96, "DevBlock layout");
 
 // A unit of work: rows [start, start+count) (forward) or redundant columns
 // [start, start+count) (adjoint) of block `blk`.
 struct Tile {
-  int32_t blk, start, count, pad;
+  int32_t blk, start, count;
+  int32_t pad;  // forward split tiles: (group << 8) | split; -1 otherwise
 };
 
 // Adjoint group-sum piece: dst[dst_off + i] = sum_r part[rd[rd_begin + r] + i].
@@ -64,13 +66,18 @@ struct Ctx {  // per-launch pointers
   void *part;      // partial pool
   const void *fin; // f input (adjoint)
   void *fout;      // f output (forward)
+  void *fsplit;    // forward split-K partial rows
+  int *fcount;     // forward split-K arrival counters (zero between applies)
   int64_t m, n, Zt, Pt;  // Zt/Pt: workspace entries per RHS (layout [entry][rhs])
   int nrhs;
 };
 
 constexpr int FWD_ROWS = 64;     // rows per forward tile (2 per lane)
 constexpr int FWD_THREADS = 128; // 4 warps split the columns
-constexpr int ADJ_COLS = 32;     // redundant columns per adjoint tile (8 per warp)
+constexpr int ADJ_COLS = 32;     // redundant columns per adjoint tile, complex (8 per warp)
+constexpr int ADJ_COLS_REAL = 64;  // ... real (16 per warp)
+template <class S>
+__host__ __device__ constexpr int adj_cols() { return sizeof(S) == 16 ? ADJ_COLS : ADJ_COLS_REAL; }
 constexpr int ADJ_THREADS = 128;
 constexpr int ADJ_RCH = 256;     // adjoint rows staged in smem per pass
 constexpr int MMA_COLS = 64;     // redundant columns per multi-RHS adjoint tile

@@ -36,6 +36,7 @@ struct Tr<double> {
   static __device__ __forceinline__ double shfl_xor(double v, int s) {
     return __shfl_xor_sync(FULL, v, s);
   }
+  static __device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
   static __device__ __forceinline__ double ldT(const double *p) {
     double v;
     asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
@@ -69,6 +70,7 @@ struct Tr<double2> {
   static __device__ __forceinline__ double2 shfl_xor(double2 v, int s) {
     return make_double2(__shfl_xor_sync(FULL, v.x, s), __shfl_xor_sync(FULL, v.y, s));
   }
+  static __device__ __forceinline__ double2 ldcg(const double2 *p) { return __ldcg(p); }
   static __device__ __forceinline__ double2 ldT(const double2 *p) {
     double2 v;
     asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
@@ -87,88 +89,106 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
 }
 
 // ------------------------------------------------------------------------
-// forward stage: one CTA per (block, 64-row tile); 4 warps split the
-// redundant columns, lane l owns rows l and l+32 of the tile.
+// forward stage (nrhs = 1): one CTA per (block, 64-row tile[, column split]);
+// 4 warps split the redundant columns, lane l owns rows l and l+32 of the
+// tile.  Stages with too few row tiles to fill the GPU split the columns of
+// large blocks (Tile.pad = group << 8 | split): every split writes its partial
+// row sums to scratch and the last CTA of the group to arrive (atomic counter)
+// adds them in split order — deterministic, no float atomics.
 // ------------------------------------------------------------------------
-template <class S, int RB>
+template <class S>
 __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Tile *__restrict__ tiles) {
   using X = Tr<S>;
   const Tile tl = tiles[blockIdx.y];
   const DevBlock B = cx.blocks[tl.blk];
-  const int rhs0 = blockIdx.x * RB;  // RHS groups of one tile run back to back: T is shared in L2
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ra = tl.start + lane, rb = tl.start + 32 + lane;
   const bool va = lane < tl.count, vb = lane + 32 < tl.count;
-  S acc_a[RB], acc_b[RB];
-#pragma unroll
-  for (int k = 0; k < RB; ++k) acc_a[k] = acc_b[k] = X::zero();
-
+  const bool split = tl.pad >= 0;
+  int jbeg = 0, jend = B.n_red;
+  if (split) {
+    const int ks = B.pad;
+    const int chunk = ((B.n_red + ks - 1) / ks + 31) & ~31;
+    jbeg = (tl.pad & 255) * chunk;
+    jend = min(B.n_red, jbeg + chunk);
+  }
+  S acc_a = X::zero(), acc_b = X::zero();
   const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
   const int64_t ld = B.r_out;
-  for (int j0 = warp * 32; j0 < B.n_red; j0 += FWD_THREADS) {
+  for (int j0 = jbeg + warp * 32; j0 < jend; j0 += FWD_THREADS) {
     const int j = j0 + lane;
-    S xr[RB];
-#pragma unroll
-    for (int k = 0; k < RB; ++k) xr[k] = X::zero();
-    if (j < B.n_red) {
+    S xr = X::zero();
+    if (j < jend) {
       const int q = (B.flags & F_RED_IOTA) ? j : cx.idx[B.red_off + j];
-#pragma unroll
-      for (int k = 0; k < RB; ++k)
-        if (rhs0 + k < cx.nrhs) xr[k] = in_value<S>(cx, B, q, rhs0 + k);
+      xr = in_value<S>(cx, B, q, 0);
     }
-    const int jn = min(32, B.n_red - j0);
+    const int jn = min(32, jend - j0);
     const S *col = T + (int64_t)j0 * ld;
     if (jn == 32) {
 #pragma unroll 8
       for (int jj = 0; jj < 32; ++jj) {
         const S ta = va ? X::ldT(col + (int64_t)jj * ld + ra) : X::zero();
         const S tb = vb ? X::ldT(col + (int64_t)jj * ld + rb) : X::zero();
-#pragma unroll
-        for (int k = 0; k < RB; ++k) {
-          const S x = X::shfl(xr[k], jj);
-          X::fma(acc_a[k], ta, x);
-          X::fma(acc_b[k], tb, x);
-        }
+        const S x = X::shfl(xr, jj);
+        X::fma(acc_a, ta, x);
+        X::fma(acc_b, tb, x);
       }
     } else {
       for (int jj = 0; jj < jn; ++jj) {
         const S ta = va ? X::ldT(col + (int64_t)jj * ld + ra) : X::zero();
         const S tb = vb ? X::ldT(col + (int64_t)jj * ld + rb) : X::zero();
-#pragma unroll
-        for (int k = 0; k < RB; ++k) {
-          const S x = X::shfl(xr[k], jj);
-          X::fma(acc_a[k], ta, x);
-          X::fma(acc_b[k], tb, x);
-        }
+        const S x = X::shfl(xr, jj);
+        X::fma(acc_a, ta, x);
+        X::fma(acc_b, tb, x);
       }
     }
   }
-  __shared__ S red[FWD_THREADS / 32][FWD_ROWS][RB];
-#pragma unroll
-  for (int k = 0; k < RB; ++k) {
-    red[warp][lane][k] = acc_a[k];
-    red[warp][lane + 32][k] = acc_b[k];
-  }
+  __shared__ S red[FWD_THREADS / 32][FWD_ROWS];
+  __shared__ int last;
+  red[warp][lane] = acc_a;
+  red[warp][lane + 32] = acc_b;
   __syncthreads();
-  for (int e = threadIdx.x; e < FWD_ROWS * RB; e += FWD_THREADS) {
-    const int i = e % FWD_ROWS, k = e / FWD_ROWS;
-    const int r = rhs0 + k;
-    if (i >= tl.count || r >= cx.nrhs) continue;
-    S s = red[0][i][k];
+  S *scratch = static_cast<S *>(cx.fsplit);
+  const int grp = tl.pad >> 8;
+  if (split) {
+    for (int i = threadIdx.x; i < FWD_ROWS; i += FWD_THREADS) {
+      S sum = red[0][i];
 #pragma unroll
-    for (int w = 1; w < FWD_THREADS / 32; ++w) s = X::add(s, red[w][i][k]);
+      for (int w = 1; w < FWD_THREADS / 32; ++w) sum = X::add(sum, red[w][i]);
+      scratch[((int64_t)grp * B.pad + (tl.pad & 255)) * FWD_ROWS + i] = sum;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(cx.fcount + grp, 1) == B.pad - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+  }
+  for (int i = threadIdx.x; i < FWD_ROWS; i += FWD_THREADS) {
+    if (i >= tl.count) continue;
+    S s;
+    if (split) {
+      s = X::zero();
+      for (int k = 0; k < B.pad; ++k) {
+        const S *p = scratch + ((int64_t)grp * B.pad + k) * FWD_ROWS + i;
+        s = X::add(s, X::ldcg(p));
+      }
+    } else {
+      s = red[0][i];
+#pragma unroll
+      for (int w = 1; w < FWD_THREADS / 32; ++w) s = X::add(s, red[w][i]);
+    }
     const int row = tl.start + i;
     if (row < B.n_skel) {
       const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
-      s = X::add(s, in_value<S>(cx, B, q, r));
+      s = X::add(s, in_value<S>(cx, B, q, 0));
     }
-    if (B.flags & F_OUT_F) {
-      const int64_t j = cx.perm[B.out_off + row];
-      static_cast<S *>(cx.fout)[r * cx.n + j] = s;
-    } else {
-      static_cast<S *>(cx.z)[(B.out_off + row) * cx.nrhs + r] = s;
-    }
+    if (B.flags & F_OUT_F)
+      static_cast<S *>(cx.fout)[cx.perm[B.out_off + row]] = s;
+    else
+      static_cast<S *>(cx.z)[B.out_off + row] = s;
   }
+  if (split && threadIdx.x == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
 }
 
 // adjoint input z[i] of a block (its zpool slot, or f through perm_x for the leaf stage)
@@ -187,7 +207,8 @@ template <class S, int RB>
 __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Tile *__restrict__ tiles,
                                                          int from_f) {
   using X = Tr<S>;
-  constexpr int CPW = ADJ_COLS / (ADJ_THREADS / 32);  // columns per warp = 8
+  // columns per warp: 8 complex / 16 real (same 128 bytes in flight per lane per row step)
+  constexpr int CPW = adj_cols<S>() / (ADJ_THREADS / 32);
   const Tile tl = tiles[blockIdx.y];
   const DevBlock B = cx.blocks[tl.blk];
   const int rhs0 = blockIdx.x * RB;
@@ -269,7 +290,9 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Ti
 // one contiguous 512-byte LDS.128 per warp (no bank conflicts).  Complex
 // products are 4 real MMAs (re/im planes of the same fragments).
 // ------------------------------------------------------------------------
-constexpr int MM_BM = 64, MM_BK = 16, MM_THREADS = 128;
+constexpr int MM_BM = 64, MM_THREADS = 128;
+template <class S>
+__host__ __device__ constexpr int mm_bk() { return sizeof(S) == 16 ? 16 : 32; }
 
 __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b) {
   asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
@@ -316,9 +339,10 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
   constexpr bool CPLX = PL::cplx;
   constexpr bool G3 = CPLX && M3;
   constexpr int NRT = 8 * NT;
-  constexpr int KS = MM_BK / 4;          // k4 steps per chunk
+  constexpr int BK = mm_bk<S>();          // K chunk: 16 complex / 32 real (16 KB of factor tile)
+  constexpr int KS = BK / 4;             // k4 steps per chunk
   constexpr int AW = MM_BM / 16;         // warps along M
-  constexpr int B_PER_T = MM_BK * NRT / MM_THREADS;
+  constexpr int B_PER_T = BK * NRT / MM_THREADS;
   constexpr int A_CH = KS * AW * 2 * 32; // scalars per A chunk (fragment order [k4][w][hi][lane])
   constexpr int B_CH = KS * NT * 32;     // scalars per B chunk ([k4][t][lane])
   // two-stage ring of fragment-ordered operand buffers.  Static shared
@@ -336,7 +360,7 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
   const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
   const int64_t ld = B.r_out;
   const int K = ADJ ? B.r_out : B.n_red;
-  const int nchunks = (K + MM_BK - 1) / MM_BK;
+  const int nchunks = (K + BK - 1) / BK;
   const bool red_iota = (B.flags & F_RED_IOTA) != 0;
 
   // Operand staging.  Thread e writes fragment slot e (contiguous, conflict-free
@@ -344,10 +368,10 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
   // m = 16 w + 8 hi + gid and k = 4 k4 + tig, so a warp reads 4 (forward) or 8
   // (adjoint) fully used 128/64-byte global segments.
   auto load_A = [&](int kc) {
-    const int kb = kc * MM_BK;
+    const int kb = kc * BK;
     S *dst = As + (kc % NB) * A_CH;
 #pragma unroll
-    for (int i = 0; i < MM_BM * MM_BK / MM_THREADS; ++i) {
+    for (int i = 0; i < MM_BM * BK / MM_THREADS; ++i) {
       const int e = threadIdx.x + MM_THREADS * i;
       const int tig_ = e & 3, gid_ = (e >> 2) & 7, hi = (e >> 5) & 1, w = (e >> 6) & (AW - 1), k4 = e >> 8;
       const int m = w * 16 + hi * 8 + gid_, k = k4 * 4 + tig_;
@@ -361,7 +385,7 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
   int qreg[B_PER_T];
   auto load_q = [&](int kc) {
     if (ADJ) return;
-    const int kb = kc * MM_BK;
+    const int kb = kc * BK;
 #pragma unroll
     for (int i = 0; i < B_PER_T; ++i) {
       const int e = threadIdx.x + MM_THREADS * i;
@@ -371,7 +395,7 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
   };
   S breg[B_PER_T];
   auto load_B = [&](int kc) {
-    const int kb = kc * MM_BK;
+    const int kb = kc * BK;
 #pragma unroll
     for (int i = 0; i < B_PER_T; ++i) {
       const int e = threadIdx.x + MM_THREADS * i;
@@ -560,7 +584,7 @@ template <class S>
 void fwd_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
     const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
-    fwd_kernel<S, 1><<<dim3(1, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
+    fwd_kernel<S><<<dim3(1, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
   }
 }
 

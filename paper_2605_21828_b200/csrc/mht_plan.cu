@@ -92,13 +92,17 @@ struct mht_plan {
   int32_t *d_idx = nullptr;
   int32_t *d_perm = nullptr;
   DevBlock *d_blocks = nullptr;
-  Tile *d_fwd = nullptr;
+  Tile *d_fwd = nullptr;   // 64-row tiles (multi-RHS DMMA path)
+  Tile *d_fwd1 = nullptr;  // nrhs = 1 tiles, with column splits on low-parallelism stages
+  void *d_fsplit = nullptr;
+  int *d_fcount = nullptr;
   Tile *d_adj = nullptr;
   Tile *d_adjm = nullptr;
   Piece *d_pieces = nullptr;
   int64_t *d_rd = nullptr;
 
-  std::vector<Range> fwd, adj, adjm, pieces;  // per stage 0..L+1
+  std::vector<Range> fwd, fwd1, adj, adjm, pieces;  // per stage 0..L+1
+  int64_t n_split_groups = 0;
   Range cpieces;
   std::vector<int64_t> stage_coef_bytes;
   std::vector<int32_t> stage_nmat;
@@ -124,7 +128,7 @@ struct mht_plan {
     clear_graphs();
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
-    for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd,
+    for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd, (void *)d_fwd1, d_fsplit, (void *)d_fcount,
                     (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, d_z, d_part, d_hc, d_hf})
       if (p) cudaFree(p);
   }
@@ -448,22 +452,23 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
     const int s = block_stage[i];
     for (int r0 = 0; r0 < D.r_out; r0 += FWD_ROWS) {
       int cnt = std::min(FWD_ROWS, D.r_out - r0);
-      ft[s].push_back({(int64_t)cnt * (D.n_red + 4), Tile{i, r0, cnt, 0}});
+      ft[s].push_back({(int64_t)cnt * (D.n_red + 4), Tile{i, r0, cnt, -1}});
     }
     if (D.n_red == 0) {
-      amt[s].push_back({(int64_t)D.r_out + D.n_skel, Tile{i, 0, 0, 0}});
+      amt[s].push_back({(int64_t)D.r_out + D.n_skel, Tile{i, 0, 0, -1}});
     } else {
       for (int c0 = 0; c0 < D.n_red; c0 += MMA_COLS) {
         int cnt = std::min(MMA_COLS, D.n_red - c0);
-        amt[s].push_back({(int64_t)cnt * (D.r_out + 4) + (c0 == 0 ? D.n_skel : 0), Tile{i, c0, cnt, 0}});
+        amt[s].push_back({(int64_t)cnt * (D.r_out + 4) + (c0 == 0 ? D.n_skel : 0), Tile{i, c0, cnt, -1}});
       }
     }
     if (D.n_red == 0) {
-      at[s].push_back({(int64_t)D.r_out + D.n_skel, Tile{i, 0, 0, 0}});
+      at[s].push_back({(int64_t)D.r_out + D.n_skel, Tile{i, 0, 0, -1}});
     } else {
-      for (int c0 = 0; c0 < D.n_red; c0 += ADJ_COLS) {
-        int cnt = std::min(ADJ_COLS, D.n_red - c0);
-        at[s].push_back({(int64_t)cnt * (D.r_out + 4) + (c0 == 0 ? D.n_skel : 0), Tile{i, c0, cnt, 0}});
+      const int acols = P->cplx ? ADJ_COLS : ADJ_COLS_REAL;
+      for (int c0 = 0; c0 < D.n_red; c0 += acols) {
+        int cnt = std::min(acols, D.n_red - c0);
+        at[s].push_back({(int64_t)cnt * (D.r_out + 4) + (c0 == 0 ? D.n_skel : 0), Tile{i, c0, cnt, -1}});
       }
     }
   }
@@ -485,6 +490,51 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
     P->adjm[s] = Range{(int32_t)adjm_all.size(), (int32_t)amt[s].size()};
     for (auto &x : amt[s]) adjm_all.push_back(x.second);
   }
+
+  // ------------------------------------------------ nrhs = 1 forward split-K
+  // A stage with fewer than FWD1_TARGET row tiles leaves SMs idle; split the
+  // columns of its large blocks (>= 256 columns per split) to reach the target.
+  const int FWD1_TARGET = prop.multiProcessorCount * 6;
+  std::vector<Tile> fwd1_all;
+  P->fwd1.assign(L + 2, Range{});
+  int64_t split_scalars = 0;
+  int32_t groups = 0;
+  for (int s = 0; s < L + 2; ++s) {
+    const int nt = (int)ft[s].size();
+    std::vector<std::pair<int64_t, Tile>> lst;
+    for (auto &x : ft[s]) {
+      DevBlock &D = blocks[x.second.blk];
+      int ks = 1;
+      if (nt > 0 && nt < FWD1_TARGET && D.n_red >= 512) {
+        ks = (FWD1_TARGET + nt - 1) / nt;
+        ks = std::min(ks, D.n_red / 256);
+        ks = std::min(ks, 255);
+      }
+      if (ks <= 1) {
+        lst.push_back(x);
+        continue;
+      }
+      D.pad = ks;  // same split count for every row tile of the block
+    }
+    for (auto &x : ft[s]) {
+      const DevBlock &D = blocks[x.second.blk];
+      if (D.pad <= 1) continue;
+      const int ks = D.pad;
+      const int chunk = ((D.n_red + ks - 1) / ks + 31) & ~31;
+      for (int k = 0; k < ks; ++k) {
+        const int cols = std::max(0, std::min(D.n_red, (k + 1) * chunk) - k * chunk);
+        Tile t = x.second;
+        t.pad = (groups << 8) | k;
+        lst.push_back({(int64_t)t.count * (cols + 4), t});
+      }
+      split_scalars += (int64_t)ks * FWD_ROWS;
+      ++groups;
+    }
+    std::stable_sort(lst.begin(), lst.end(), by_cost);
+    P->fwd1[s] = Range{(int32_t)fwd1_all.size(), (int32_t)lst.size()};
+    for (auto &x : lst) fwd1_all.push_back(x.second);
+  }
+  P->n_split_groups = groups;
 
   // ------------------------------------------------ adjoint group-sum pieces
   // Readers: every materialised block's input segments.  For a source range
@@ -591,6 +641,11 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
   if ((st = upload(&P->d_perm, perm, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_blocks, blocks, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_fwd, fwd_all, P->device_bytes)) != MHT_OK) return st;
+  if ((st = upload(&P->d_fwd1, fwd1_all, P->device_bytes)) != MHT_OK) return st;
+  CUDA_TRY(cudaMalloc(&P->d_fsplit, (size_t)std::max<int64_t>(split_scalars, 1) * P->ssz));
+  CUDA_TRY(cudaMalloc((void **)&P->d_fcount, (size_t)std::max<int64_t>(groups, 1) * sizeof(int)));
+  CUDA_TRY(cudaMemset(P->d_fcount, 0, (size_t)std::max<int64_t>(groups, 1) * sizeof(int)));
+  P->device_bytes += split_scalars * (int64_t)P->ssz + groups * 4;
   if ((st = upload(&P->d_adj, adj_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_adjm, adjm_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_pieces, pieces_all, P->device_bytes)) != MHT_OK) return st;
@@ -621,6 +676,8 @@ Ctx make_ctx(mht_plan *P, int nrhs) {
   cx.blocks = P->d_blocks;
   cx.z = P->d_z;
   cx.part = P->d_part;
+  cx.fsplit = P->d_fsplit;
+  cx.fcount = P->d_fcount;
   cx.m = P->m;
   cx.n = P->n;
   cx.Zt = P->Zt;
@@ -662,9 +719,9 @@ mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs) {
   cx.c = c;
   cx.fout = f;
   for (int s = 0; s < P->L + 2; ++s)
-    timed(P, 0, s, nrhs, P->fwd[s].count, [&] {
+    timed(P, 0, s, nrhs, nrhs == 1 ? P->fwd1[s].count : P->fwd[s].count, [&] {
       if (nrhs == 1)
-        launch_fwd(P->cplx, cx, P->d_fwd + P->fwd[s].off, P->fwd[s].count, P->stream);
+        launch_fwd(P->cplx, cx, P->d_fwd1 + P->fwd1[s].off, P->fwd1[s].count, P->stream);
       else
         launch_mma(P->cplx, false, cx, P->d_fwd + P->fwd[s].off, P->fwd[s].count, false, P->stream);
     });

@@ -82,3 +82,32 @@ def test_device_builder_plan_accuracy(oracle_lib, tmp_path, family):
     f = P.apply(c)
     for r in range(2):
         assert np.linalg.norm(f[r] - ref[r]) / np.linalg.norm(ref[r]) <= 10 * tol
+
+
+@pytest.mark.parametrize("builder", ["cpu", "device"])
+def test_mesh_plan_fiedler(oracle_lib, tmp_path, builder):
+    """configs[3] pipeline at small size: torus mesh, stored eigenvectors,
+    Fiedler-tree rows (uneven leaves), plan within 10 tol of the dense sum."""
+    from mht_inputs import mesh as mm
+    from paper_2605_21828_b200.precompute import build_plan
+    from paper_2605_21828_b200.precompute.basis import DenseBasis
+    from paper_2605_21828_b200.precompute.fiedler import fiedler_tree
+
+    V, F = mm.torus_mesh(32, 16, sigma=0.01)
+    lam, Phi, mass, _ = mm.mesh_eigenbasis(V, F, 256)
+    L, tol = 2, 1e-8
+    perm, sp = fiedler_tree(V, F, L)
+    path = str(tmp_path / f"mesh_{builder}.plan")
+    if builder == "cpu":
+        build_plan(DenseBasis(Phi), perm, sp, freq_tree(256, L), L, tol, path, workers=2, log=None)
+    else:
+        build_plan_gpu(TorchTableBasis(torch.as_tensor(Phi), np.float64), perm, sp, freq_tree(256, L), L, tol,
+                       path, device="cpu", log=None)
+    P = oracle_lib.Plan(path)
+    c = mi.real_gaussian(2, 256, 1)
+    f, fd = P.apply(c), oracle_lib.dense_synth(Phi, c)
+    y = mi.real_gaussian(2, V.shape[0], 2)
+    a, ad = P.adjoint(y), oracle_lib.dense_analysis(Phi, y)
+    for r in range(2):
+        assert np.linalg.norm(f[r] - fd[r]) / np.linalg.norm(fd[r]) <= 10 * tol
+        assert np.linalg.norm(a[r] - ad[r]) / np.linalg.norm(ad[r]) <= 10 * tol

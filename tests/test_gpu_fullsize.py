@@ -79,3 +79,15 @@ def test_config3_sphere_65536_full_size(gpu, oracle_lib):
     _run(gpu, oracle_lib, w,
          lambda rows, c: oracle_lib.sphere_synth(th[rows], ph[rows], lmax, c),
          dense_cols)
+
+
+def test_config4_torus_mesh_full_size(gpu, oracle_lib):
+    """configs[3]: torus mesh n = 32,768, m = 2,048 stored eigenvectors,
+    Fiedler-tree rows, tol 1e-8, nrhs 1 and 64."""
+    from mht_inputs import mesh as mm
+
+    w = mi.WORKLOADS["c4"]
+    _, _, _, Phi, _ = mm.torus_workload_inputs(w.extra["nu"], w.extra["nv"], w.m)
+    _run(gpu, oracle_lib, w,
+         lambda rows, c: oracle_lib.dense_synth(Phi[rows], c),
+         lambda cols, y: oracle_lib.dense_analysis(Phi[:, cols], y))

@@ -220,3 +220,20 @@ def test_cuda_graph_replay_matches_eager(gpu, plans):
     for nrhs in (1, 5, 32):
         assert torch.equal(outs[(1, nrhs)][0], outs[(0, nrhs)][0])
         assert torch.equal(outs[(1, nrhs)][1], outs[(0, nrhs)][1])
+
+
+def test_forward_split_k_low_parallelism(gpu, oracle_lib, plans):
+    """A stage with few row tiles and long rows takes the split-column path
+    (partials + last-CTA fixup); results match O2 and stay bitwise
+    deterministic across repeated applies."""
+    rng = np.random.default_rng(11)
+    n, m, L = 256, 4096, 2
+    Phi = rng.standard_normal((n, m))
+    path = _dense_plan(plans, Phi, L, 1e-12, "split_k")
+    w = mi.Workload("sk", "mesh", n, m, "float64", 1e-12, L)
+    P, O = check_plan(gpu, oracle_lib, path, w, (1, 3))
+    c = torch.from_numpy(rng.standard_normal((1, m))).cuda()
+    f1, f2 = P.apply(c), P.apply(c)
+    assert torch.equal(f1, f2)
+    fd = torch.from_numpy(Phi).cuda() @ c[0]
+    assert (torch.linalg.vector_norm(f1[0] - fd) / torch.linalg.vector_norm(fd)).item() < 1e-11
