@@ -309,18 +309,25 @@ def main():
     dom = max(((k, v) for k, v in per.items() if k[0] in ("fwd", "adj")), key=lambda kv: kv[1][0])
     (dkind, dr), (dms, dn) = dom
     per_launch_ms = dms / dn
+    traffic = _traffic(w.name, f"{dkind}@{dr}")
     if dr == 1:
         alg = (coef_bytes + (w.m + w.n) * sb) / (dn / args.steps)        # bytes per launch (average)
         achieved = alg / (per_launch_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "algorithmic_bytes_per_launch": alg,
                 "kernel": f"{dkind}_kernel nrhs=1", "peak_source": peaks["hbm_src"]}
     else:
+        # the multi-RHS stages run on the FP64 tensor pipe (DMMA): its own measured peak
         alg = (8 if P.is_complex else 2) * entries * dr / (dn / args.steps)
         achieved = alg / (per_launch_ms / 1e3) / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["fp64_tflops"], "traffic": None,
-                "kernel": f"{dkind}_kernel nrhs={dr} (FP64 FMA pipe)", "peak_source": peaks["fp64_src"]}
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["dmma_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["dmma_tflops"], "traffic": traffic, "algorithmic_flops_per_launch": alg,
+                "kernel": f"mma_kernel {dkind} nrhs={dr} (DMMA m16n8k4 f64)", "peak_source": peaks["dmma_src"]}
+        if P.is_complex:
+            roof["note"] = ("achieved counts 8 real flops per complex multiply-add (algorithmic); the kernel "
+                            "issues 3 real DMMA products per complex product (Gauss), so pipe work is 3/4 of that")
+    if traffic is not None:
+        roof["traffic_source"] = _traffic_src(w.name)
     roof["per_launch_ms"] = per_launch_ms
     roof["launches_per_apply"] = dn / args.steps
 
@@ -408,11 +415,36 @@ def _peaks():
     try:
         d = json.load(open(fp))
         out["fp64_tflops"] = float(d["dfma_tflops"])
+        out["dmma_tflops"] = float(d["dmma_m16n8k4_tflops"])
         out["fp64_src"] = f"measured DFMA microbenchmark ({os.path.relpath(fp, ROOT)})"
+        out["dmma_src"] = f"measured DMMA m16n8k4 microbenchmark ({os.path.relpath(fp, ROOT)})"
     except Exception:
-        out["fp64_tflops"] = 148 * 64 * 2 * smax * 1e6 / 1e12
-        out["fp64_src"] = "derived: 148 SMs x 64 FP64 FMA/clk x 2 x sm_max_mhz"
+        out["fp64_tflops"] = out["dmma_tflops"] = 148 * 64 * 2 * smax * 1e6 / 1e12
+        out["fp64_src"] = out["dmma_src"] = "derived: 148 SMs x 64 FP64 FMA/clk x 2 x sm_max_mhz"
     return out
+
+
+def _traffic_file(workload):
+    cands = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles"))
+                   if f.endswith(f"_traffic_{workload}.json"))
+    return os.path.join(ROOT, "profiles", cands[-1]) if cands else None
+
+
+def _traffic(workload, phase):
+    """DRAM bytes per launch of the dominant phase from the committed ncu capture
+    (profiles/rNN_traffic_<workload>.json, tools/ncu_traffic.py), else None."""
+    f = _traffic_file(workload)
+    if f is None:
+        return None
+    try:
+        return json.load(open(f))["phases"][phase]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def _traffic_src(workload):
+    f = _traffic_file(workload)
+    return os.path.relpath(f, ROOT) if f else None
 
 
 if __name__ == "__main__":
