@@ -295,6 +295,21 @@ def main():
             ms, nl = P.profile_get(kind_i, -1, r)
             if nl:
                 per[(kind, r)] = (ms, nl)
+    # per-stage device time (ms per apply) of every phase, with the stage's factor bytes
+    stage_ms = {}
+    for kind_i, kind in ((0, "fwd"), (1, "adj"), (2, "sum")):
+        for r in widths:
+            row = {}
+            for s_ in range(0, P.L + 2):
+                ms, nl = P.profile_get(kind_i, s_, r)
+                if nl:
+                    row[str(s_)] = round(ms / args.steps, 4)
+            if kind == "sum":  # stage -1 (the final sums into c) = all - the per-stage ones
+                ms, nl = P.profile_get(kind_i, -1, r)
+                if nl:
+                    row["c"] = round(ms / args.steps - sum(row.values()), 4)
+            if row:
+                stage_ms[f"{kind}_nrhs{r}"] = row
     P.set_profiling(False)
     breakdown = {}
     for (kind, r), (ms, nl) in per.items():
@@ -341,8 +356,9 @@ def main():
                       "factor_fraction_of_dense": entries / (w.n * w.m),
                       "l2": ("plan larger than L2 (no flush)" if flush is None else "L2 flushed between steps")},
            "roofline": roof, "breakdown": breakdown, "clocks": clk,
-           "gpu_launches": args.steps * sum(P.info.fwd_launches if k == "fwd" else P.info.adj_launches
-                                             for k, _ in phases)}
+           "stage_ms": stage_ms, "stage_coef_bytes": {str(x["stage"]): x["coef_bytes"] for x in stats},
+           # counted: every launch of the timed region is bracketed by the library's events
+           "gpu_launches": int(sum(nl for _, nl in per.values()))}
 
     # ---- end to end through the C ABI with pinned host buffers
     if not args.no_e2e:

@@ -113,6 +113,16 @@ mht_status mht_apply_adjoint_host(mht_plan *plan, const void *f_host, void *c_ho
  * replay it on later calls with the same arguments (on = 1, default on). */
 mht_status mht_set_graphs(mht_plan *plan, int on);
 
+/* Adjoint group sums (a block row read by two transfers receives
+ * the sum of both adjoint contributions).  on = 1 (default): each consumer
+ * sums its producers' per-block partials while loading its input, so no
+ * separate reduction pass runs except the final one into c (used at nrhs = 1;
+ * multi-RHS applies always reduce first, which measured faster).  on = 0: one
+ * reduce pass per stage writes the sums to the workspace first.  Both orders
+ * add the same partials in the same order (results are bitwise identical).
+ * Synchronises the plan's stream and drops captured graphs. */
+mht_status mht_set_fused_sums(mht_plan *plan, int on);
+
 /* Block until the plan's stream is idle; returns MHT_ERR_CUDA on a fault. */
 mht_status mht_sync(mht_plan *plan);
 

@@ -35,8 +35,15 @@ struct DevBlock {
   int32_t r_out, r_in, n_skel, n_red;
   int32_t flags;
   int32_t pad;  // forward column splits (nrhs = 1), 0 = none
+  // adjoint input fused into the load: z[i] = sum_k part[rdtab[rd_off + k] + i]
+  // over the rd_cnt readers of this block's output (-1: not fusable, read z).
+  int64_t rd_off;
+  int32_t rd_cnt;
+  int32_t pad2;     // adjoint row splits (nrhs = 1), 0 = none
+  int64_t fsp_off;  // split scratch base of this block's forward row tiles (scalars)
+  int64_t asp_off;  // split scratch base of this block's adjoint column tiles (scalars)
 };
-static_assert(sizeof(DevBlock) == 96, "DevBlock layout");
+static_assert(sizeof(DevBlock) == 128, "DevBlock layout");
 
 // A unit of work: rows [start, start+count) (forward) or redundant columns
 // [start, start+count) (adjoint) of block `blk`.
@@ -68,6 +75,8 @@ struct Ctx {  // per-launch pointers
   void *fout;      // f output (forward)
   void *fsplit;    // forward split-K partial rows
   int *fcount;     // forward split-K arrival counters (zero between applies)
+  const int64_t *rdtab;  // fused adjoint sums: reader partial offsets
+  int fused;             // 1: adjoint inputs are summed from the partials on load
   int64_t m, n, Zt, Pt;  // Zt/Pt: workspace entries per RHS (layout [entry][rhs])
   int nrhs;
 };

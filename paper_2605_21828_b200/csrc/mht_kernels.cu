@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Ti
       S sum = red[0][i];
 #pragma unroll
       for (int w = 1; w < FWD_THREADS / 32; ++w) sum = X::add(sum, red[w][i]);
-      scratch[((int64_t)grp * B.pad + (tl.pad & 255)) * FWD_ROWS + i] = sum;
+      scratch[B.fsp_off + ((int64_t)(tl.start / FWD_ROWS) * B.pad + (tl.pad & 255)) * FWD_ROWS + i] = sum;
     }
     __threadfence();
     __syncthreads();
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Ti
     if (split) {
       s = X::zero();
       for (int k = 0; k < B.pad; ++k) {
-        const S *p = scratch + ((int64_t)grp * B.pad + k) * FWD_ROWS + i;
+        const S *p = scratch + B.fsp_off + ((int64_t)(tl.start / FWD_ROWS) * B.pad + k) * FWD_ROWS + i;
         s = X::add(s, X::ldcg(p));
       }
     } else {
@@ -191,28 +191,54 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Ti
   if (split && threadIdx.x == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
 }
 
-// adjoint input z[i] of a block (its zpool slot, or f through perm_x for the leaf stage)
+// adjoint input z[i] of a block: f through perm_x (leaf stage), else the group
+// sum of its readers' partials (the adjoint of a block row that
+// feeds two transfers is the sum of both), either summed here on load (fused:
+// no separate reduction pass) or read from the zpool slot reduce_kernel wrote.
+// The fused sum adds the partials in the same (reader id) order as
+// reduce_kernel, so both paths are bitwise identical.
 template <class S>
 __device__ __forceinline__ S adj_in(const Ctx &cx, const DevBlock &B, int i, int r, bool from_f) {
   if (from_f) return static_cast<const S *>(cx.fin)[r * cx.n + cx.perm[B.out_off + i]];
+  if (cx.fused && B.rd_cnt >= 0) {
+    const S *part = static_cast<const S *>(cx.part);
+    S s = Tr<S>::zero();
+    for (int k = 0; k < B.rd_cnt; ++k) s = Tr<S>::add(s, part[(cx.rdtab[B.rd_off + k] + i) * cx.nrhs + r]);
+    return s;
+  }
   return static_cast<const S *>(cx.z)[(B.out_off + i) * cx.nrhs + r];
 }
 
 // ------------------------------------------------------------------------
-// adjoint stage: one CTA per (block, 32 redundant columns); warp w owns 8
-// columns and computes their conj-dot products with z over all r_out rows
-// (rows staged through shared memory, ADJ_RCH at a time).
+// adjoint stage (nrhs = 1): one CTA per (block, 32 complex / 64 real redundant
+// columns[, row split]); warp w owns CPW columns and computes their conj-dot
+// products with z over the tile's rows (staged through shared memory,
+// ADJ_RCH at a time), reduced across lanes with shuffles.  Stages with too few
+// column tiles to fill the GPU split the rows of tall blocks (Tile.pad =
+// group << 8 | split, DevBlock.pad2 = split count): every split writes its
+// partial column sums to scratch and the last CTA of the group to arrive adds
+// them in split order (deterministic, no float atomics).
 // ------------------------------------------------------------------------
 template <class S, int RB>
 __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Tile *__restrict__ tiles,
                                                          int from_f) {
   using X = Tr<S>;
   // columns per warp: 8 complex / 16 real (same 128 bytes in flight per lane per row step)
-  constexpr int CPW = adj_cols<S>() / (ADJ_THREADS / 32);
+  constexpr int ACOLS = adj_cols<S>();
+  constexpr int CPW = ACOLS / (ADJ_THREADS / 32);
   const Tile tl = tiles[blockIdx.y];
   const DevBlock B = cx.blocks[tl.blk];
   const int rhs0 = blockIdx.x * RB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool split = tl.pad >= 0;
+  const int sidx = split ? (tl.pad & 255) : 0;
+  int rbeg = 0, rend = B.r_out;
+  if (split) {
+    const int ks = B.pad2;
+    const int chunk = ((B.r_out + ks - 1) / ks + 31) & ~31;
+    rbeg = sidx * chunk;
+    rend = min(B.r_out, rbeg + chunk);
+  }
   __shared__ S zs[ADJ_RCH][RB];
   S acc[CPW][RB];
 #pragma unroll
@@ -224,8 +250,8 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Ti
   const int cbase = tl.start + warp * CPW;
   const int cend = tl.start + tl.count;
 
-  for (int rc = 0; rc < B.r_out; rc += ADJ_RCH) {
-    const int rn = min(ADJ_RCH, B.r_out - rc);
+  for (int rc = rbeg; rc < rend; rc += ADJ_RCH) {
+    const int rn = min(ADJ_RCH, rend - rc);
     for (int e = threadIdx.x; e < rn * RB; e += ADJ_THREADS) {
       const int i = e % rn, k = e / rn;
       zs[i][k] = (rhs0 + k < cx.nrhs) ? adj_in<S>(cx, B, rc + i, rhs0 + k, from_f) : X::zero();
@@ -248,6 +274,15 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Ti
     }
     __syncthreads();
   }
+  // skeleton part: w[skel[i]] = z[i]  (written once, by the block's first tile)
+  if (tl.start == 0 && sidx == 0 && B.n_skel > 0) {
+    for (int e = threadIdx.x; e < B.n_skel * RB; e += ADJ_THREADS) {
+      const int i = e % B.n_skel, k = e / B.n_skel;
+      if (rhs0 + k >= cx.nrhs) continue;
+      const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
+      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0 + k] = adj_in<S>(cx, B, i, rhs0 + k, from_f);
+    }
+  }
   // warp reductions
 #pragma unroll
   for (int u = 0; u < CPW; ++u)
@@ -255,25 +290,43 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Ti
     for (int k = 0; k < RB; ++k)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc[u][k] = X::add(acc[u][k], X::shfl_xor(acc[u][k], o));
-  if (lane == 0) {
+  if (!split) {
+    if (lane == 0) {
 #pragma unroll
-    for (int u = 0; u < CPW; ++u) {
-      const int col = cbase + u;
-      if (col >= cend) continue;
+      for (int u = 0; u < CPW; ++u) {
+        const int col = cbase + u;
+        if (col >= cend) continue;
+        const int q = (B.flags & F_RED_IOTA) ? col : cx.idx[B.red_off + col];
+#pragma unroll
+        for (int k = 0; k < RB; ++k)
+          if (rhs0 + k < cx.nrhs) static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0 + k] = acc[u][k];
+      }
+    }
+  } else {
+    // RB == 1 here (nrhs = 1 path)
+    static_assert(RB == 1, "row splits are built for the nrhs = 1 tiles only");
+    S *scratch = static_cast<S *>(cx.fsplit);
+    const int grp = tl.pad >> 8;
+    const int64_t sbase = B.asp_off + (int64_t)(tl.start / ACOLS) * B.pad2 * ACOLS;
+    __shared__ int last;
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) scratch[sbase + (int64_t)sidx * ACOLS + warp * CPW + u] = acc[u][0];
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(cx.fcount + grp, 1) == B.pad2 - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int c = threadIdx.x; c < tl.count; c += ADJ_THREADS) {
+      S sum = X::zero();
+      for (int k = 0; k < B.pad2; ++k) sum = X::add(sum, X::ldcg(scratch + sbase + (int64_t)k * ACOLS + c));
+      const int col = tl.start + c;
       const int q = (B.flags & F_RED_IOTA) ? col : cx.idx[B.red_off + col];
-#pragma unroll
-      for (int k = 0; k < RB; ++k)
-        if (rhs0 + k < cx.nrhs) static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0 + k] = acc[u][k];
+      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0] = sum;
     }
-  }
-  // skeleton part: w[skel[i]] = z[i]  (written once, by the block's first tile)
-  if (tl.start == 0 && B.n_skel > 0) {
-    for (int e = threadIdx.x; e < B.n_skel * RB; e += ADJ_THREADS) {
-      const int i = e % B.n_skel, k = e / B.n_skel;
-      if (rhs0 + k >= cx.nrhs) continue;
-      const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
-      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0 + k] = adj_in<S>(cx, B, i, rhs0 + k, from_f);
-    }
+    if (threadIdx.x == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
   }
 }
 

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -102,6 +103,10 @@ struct mht_plan {
   int64_t *d_rd = nullptr;
 
   std::vector<Range> fwd, fwd1, adj, adjm, pieces;  // per stage 0..L+1
+  std::vector<Range> pieces_u;  // pieces of the producers that are not fused (fused mode)
+  int64_t *d_rdtab = nullptr;
+  bool fused_sum = true;        // adjoint group sums on the consumer's load (MHT_FUSED_SUM=0: off)
+  int n_unfused = 0;
   int64_t n_split_groups = 0;
   Range cpieces;
   std::vector<int64_t> stage_coef_bytes;
@@ -129,7 +134,7 @@ struct mht_plan {
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd, (void *)d_fwd1, d_fsplit, (void *)d_fcount,
-                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, d_z, d_part, d_hc, d_hf})
+                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, d_z, d_part, d_hc, d_hf})
       if (p) cudaFree(p);
   }
 };
@@ -473,6 +478,11 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
     }
   }
   std::vector<Tile> fwd_all, adj_all, adjm_all;
+  const int ADJ1_TARGET = prop.multiProcessorCount * 6;
+  int ADJ1_MIN_SPLIT = 128;
+  if (const char *e = getenv("MHT_ASPLIT_MIN")) ADJ1_MIN_SPLIT = std::max(32, atoi(e));
+  int64_t asplit_scalars = 0;
+  int32_t agroups = 0;
   P->fwd.assign(L + 2, Range{});
   P->adj.assign(L + 2, Range{});
   P->adjm.assign(L + 2, Range{});
@@ -481,11 +491,50 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
   };
   for (int s = 0; s < L + 2; ++s) {
     std::stable_sort(ft[s].begin(), ft[s].end(), by_cost);
-    std::stable_sort(at[s].begin(), at[s].end(), by_cost);
     P->fwd[s] = Range{(int32_t)fwd_all.size(), (int32_t)ft[s].size()};
     for (auto &x : ft[s]) fwd_all.push_back(x.second);
-    P->adj[s] = Range{(int32_t)adj_all.size(), (int32_t)at[s].size()};
-    for (auto &x : at[s]) adj_all.push_back(x.second);
+    // nrhs = 1 adjoint row splits: a stage with fewer column tiles than
+    // ADJ1_TARGET splits the rows of its tall blocks (>= ADJ1_MIN_SPLIT rows
+    // per split); partial column sums are combined by the group's last CTA.
+    {
+      const int nt = (int)at[s].size();
+      std::vector<std::pair<int64_t, Tile>> lst;
+      for (auto &x : at[s]) {
+        DevBlock &D = blocks[x.second.blk];
+        int ks = 1;
+        if (nt > 0 && nt < ADJ1_TARGET && D.n_red > 0 && D.r_out >= 2 * ADJ1_MIN_SPLIT) {
+          ks = (ADJ1_TARGET + nt - 1) / nt;
+          ks = std::min(ks, D.r_out / ADJ1_MIN_SPLIT);
+          ks = std::min(ks, 255);
+        }
+        if (ks <= 1 || x.second.count == 0) {
+          lst.push_back(x);
+          continue;
+        }
+        if (D.pad2 == 0) {  // first column tile of the block: reserve its scratch
+          D.pad2 = ks;
+          D.asp_off = asplit_scalars;
+          const int acols = P->cplx ? ADJ_COLS : ADJ_COLS_REAL;
+          asplit_scalars += (int64_t)((D.n_red + acols - 1) / acols) * ks * acols;
+        }
+        const int chunk = ((D.r_out + ks - 1) / ks + 31) & ~31;
+        for (int k = 0; k < ks; ++k) {
+          const int rows = std::max(0, std::min(D.r_out, (k + 1) * chunk) - k * chunk);
+          Tile t = x.second;
+          t.pad = (agroups << 8) | k;
+          lst.push_back({(int64_t)t.count * (rows + 4) + (k == 0 && t.start == 0 ? D.n_skel : 0), t});
+        }
+        ++agroups;
+      }
+      // a block is split in every one of its column tiles or in none
+      for (auto &x : lst) {
+        const DevBlock &D = blocks[x.second.blk];
+        if (D.pad2 > 1 && x.second.pad < 0 && x.second.count > 0) return fail(MHT_ERR_FORMAT, "adjoint split tiling");
+      }
+      std::stable_sort(lst.begin(), lst.end(), by_cost);
+      P->adj[s] = Range{(int32_t)adj_all.size(), (int32_t)lst.size()};
+      for (auto &x : lst) adj_all.push_back(x.second);
+    }
     std::stable_sort(amt[s].begin(), amt[s].end(), by_cost);
     P->adjm[s] = Range{(int32_t)adjm_all.size(), (int32_t)amt[s].size()};
     for (auto &x : amt[s]) adjm_all.push_back(x.second);
@@ -493,8 +542,11 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
 
   // ------------------------------------------------ nrhs = 1 forward split-K
   // A stage with fewer than FWD1_TARGET row tiles leaves SMs idle; split the
-  // columns of its large blocks (>= 256 columns per split) to reach the target.
+  // columns of its blocks (>= FWD1_MIN_SPLIT columns per split) to reach the target.
   const int FWD1_TARGET = prop.multiProcessorCount * 6;
+  // columns per split: env MHT_SPLIT_MIN (experiments), default 64
+  int FWD1_MIN_SPLIT = 64;
+  if (const char *e = getenv("MHT_SPLIT_MIN")) FWD1_MIN_SPLIT = std::max(32, atoi(e));
   std::vector<Tile> fwd1_all;
   P->fwd1.assign(L + 2, Range{});
   int64_t split_scalars = 0;
@@ -505,16 +557,20 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
     for (auto &x : ft[s]) {
       DevBlock &D = blocks[x.second.blk];
       int ks = 1;
-      if (nt > 0 && nt < FWD1_TARGET && D.n_red >= 512) {
+      if (nt > 0 && nt < FWD1_TARGET && D.n_red >= 2 * FWD1_MIN_SPLIT) {
         ks = (FWD1_TARGET + nt - 1) / nt;
-        ks = std::min(ks, D.n_red / 256);
+        ks = std::min(ks, D.n_red / FWD1_MIN_SPLIT);
         ks = std::min(ks, 255);
       }
       if (ks <= 1) {
         lst.push_back(x);
         continue;
       }
-      D.pad = ks;  // same split count for every row tile of the block
+      if (D.pad == 0) {  // first row tile of the block: reserve its scratch
+        D.pad = ks;        // same split count for every row tile of the block
+        D.fsp_off = split_scalars;
+        split_scalars += (int64_t)((D.r_out + FWD_ROWS - 1) / FWD_ROWS) * ks * FWD_ROWS;
+      }
     }
     for (auto &x : ft[s]) {
       const DevBlock &D = blocks[x.second.blk];
@@ -527,7 +583,6 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
         t.pad = (groups << 8) | k;
         lst.push_back({(int64_t)t.count * (cols + 4), t});
       }
-      split_scalars += (int64_t)ks * FWD_ROWS;
       ++groups;
     }
     std::stable_sort(lst.begin(), lst.end(), by_cost);
@@ -549,19 +604,44 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
     if (D.seg_len[0] > 0) readers.push_back({D.seg_src[0], D.seg_off[0], D.seg_len[0], D.part_off});
     if (D.seg_len[1] > 0) readers.push_back({D.seg_src[1], D.seg_off[1], D.seg_len[1], D.part_off + D.seg_len[0]});
   }
+  // Fused group sums: a zpool producer whose output range is covered only by
+  // readers that contain it whole gets the list of their partial offsets (in
+  // reader-id order, the order reduce_kernel sums in); its consumer then sums
+  // them on load and no reduction pass runs for it.
+  std::vector<char> unfusable(blocks.size(), 0);
+  std::vector<std::vector<int64_t>> rdl(blocks.size());
+  {
+    std::map<int64_t, int> prod_at;  // zpool out_off -> producer block
+    for (int i = 0; i < (int)blocks.size(); ++i)
+      if (!(blocks[i].flags & F_OUT_F) && blocks[i].r_out > 0) prod_at[blocks[i].out_off] = i;
+    for (const Rd &r : readers) {
+      if (r.src != SRC_Z) continue;
+      auto it = prod_at.lower_bound(r.start);  // first producer starting at or after the reader
+      if (it != prod_at.begin()) {              // a producer straddling the reader's start
+        auto pv = std::prev(it);
+        if (r.start < pv->first + blocks[pv->second].r_out) unfusable[pv->second] = 1;
+      }
+      for (; it != prod_at.end() && it->first < r.start + r.len; ++it) {
+        if (it->first + blocks[it->second].r_out > r.start + r.len) unfusable[it->second] = 1;
+        else rdl[it->second].push_back(r.pstart + (it->first - r.start));
+      }
+    }
+  }
   // producer regions: c = [0, m) ("stage -1"), zpool slots of stage s <= L
   struct Region {
     int32_t src, stage;
     int64_t start, len;
+    int blk;  // producer block (-1: the user's c)
   };
   std::vector<Region> regions;
-  regions.push_back({SRC_C, -1, 0, P->m});
+  regions.push_back({SRC_C, -1, 0, P->m, -1});
   for (int i = 0; i < (int)blocks.size(); ++i) {
     const DevBlock &D = blocks[i];
-    if (!(D.flags & F_OUT_F) && D.r_out > 0) regions.push_back({SRC_Z, block_stage[i], D.out_off, D.r_out});
+    if (!(D.flags & F_OUT_F) && D.r_out > 0) regions.push_back({SRC_Z, block_stage[i], D.out_off, D.r_out, i});
   }
   std::vector<std::vector<Piece>> pcs(L + 3);  // index stage+1 (0 = c)
   std::vector<std::vector<std::vector<int64_t>>> pcs_rd(L + 3);
+  std::vector<std::vector<char>> pcs_keep(L + 3);  // piece still needed in fused mode
   for (int src : {SRC_C, SRC_Z}) {
     std::vector<int64_t> cuts;
     std::vector<const Region *> regs;
@@ -615,25 +695,52 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
         pc.rd_count = (int32_t)rr.size();
         pcs[slot].push_back(pc);
         pcs_rd[slot].push_back(std::move(rr));
+        pcs_keep[slot].push_back(regs[ri]->blk < 0 || unfusable[regs[ri]->blk]);
       }
     }
   }
   std::vector<Piece> pieces_all;
   std::vector<int64_t> rd_all;
   P->pieces.assign(L + 2, Range{});
+  P->pieces_u.assign(L + 2, Range{});
   for (int slot = 0; slot < L + 3; ++slot) {
-    Range rg{(int32_t)pieces_all.size(), (int32_t)pcs[slot].size()};
-    for (size_t k = 0; k < pcs[slot].size(); ++k) {
-      Piece pc = pcs[slot][k];
-      pc.rd_begin = (int64_t)rd_all.size();
-      rd_all.insert(rd_all.end(), pcs_rd[slot][k].begin(), pcs_rd[slot][k].end());
-      pieces_all.push_back(pc);
+    // all pieces of the slot (unfused mode), then the unfused producers' pieces
+    // again as their own range (fused mode)
+    for (int pass = 0; pass < (slot == 0 ? 1 : 2); ++pass) {
+      Range rg{(int32_t)pieces_all.size(), 0};
+      for (size_t k = 0; k < pcs[slot].size(); ++k) {
+        if (pass == 1 && !pcs_keep[slot][k]) continue;
+        Piece pc = pcs[slot][k];
+        pc.rd_begin = (int64_t)rd_all.size();
+        rd_all.insert(rd_all.end(), pcs_rd[slot][k].begin(), pcs_rd[slot][k].end());
+        pieces_all.push_back(pc);
+        ++rg.count;
+      }
+      if (slot == 0)
+        P->cpieces = rg;
+      else if (pass == 0)
+        P->pieces[slot - 1] = rg;
+      else
+        P->pieces_u[slot - 1] = rg;
     }
-    if (slot == 0)
-      P->cpieces = rg;
-    else
-      P->pieces[slot - 1] = rg;
   }
+  // per-block fused reader lists
+  std::vector<int64_t> rdtab;
+  P->n_unfused = 0;
+  for (int i = 0; i < (int)blocks.size(); ++i) {
+    DevBlock &D = blocks[i];
+    D.rd_off = (int64_t)rdtab.size();
+    if (D.flags & F_OUT_F) {
+      D.rd_cnt = 0;
+    } else if (unfusable[i]) {
+      D.rd_cnt = -1;
+      ++P->n_unfused;
+    } else {
+      D.rd_cnt = (int32_t)rdl[i].size();
+      rdtab.insert(rdtab.end(), rdl[i].begin(), rdl[i].end());
+    }
+  }
+  if (const char *e = getenv("MHT_FUSED_SUM")) P->fused_sum = strcmp(e, "0") != 0;
 
   // ------------------------------------------------ upload
   mht_status st;
@@ -642,14 +749,21 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
   if ((st = upload(&P->d_blocks, blocks, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_fwd, fwd_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_fwd1, fwd1_all, P->device_bytes)) != MHT_OK) return st;
-  CUDA_TRY(cudaMalloc(&P->d_fsplit, (size_t)std::max<int64_t>(split_scalars, 1) * P->ssz));
-  CUDA_TRY(cudaMalloc((void **)&P->d_fcount, (size_t)std::max<int64_t>(groups, 1) * sizeof(int)));
-  CUDA_TRY(cudaMemset(P->d_fcount, 0, (size_t)std::max<int64_t>(groups, 1) * sizeof(int)));
-  P->device_bytes += split_scalars * (int64_t)P->ssz + groups * 4;
+  // split scratch + arrival counters, shared by the forward (row tiles split
+  // by columns) and the adjoint (column tiles split by rows): applies on one
+  // plan are serialised on its stream, and the last CTA of a group re-arms
+  // its counter
+  const int64_t sp_scalars = std::max<int64_t>({split_scalars, asplit_scalars, 1});
+  const int64_t sp_groups = std::max<int64_t>({(int64_t)groups, (int64_t)agroups, 1});
+  CUDA_TRY(cudaMalloc(&P->d_fsplit, (size_t)sp_scalars * P->ssz));
+  CUDA_TRY(cudaMalloc((void **)&P->d_fcount, (size_t)sp_groups * sizeof(int)));
+  CUDA_TRY(cudaMemset(P->d_fcount, 0, (size_t)sp_groups * sizeof(int)));
+  P->device_bytes += sp_scalars * (int64_t)P->ssz + sp_groups * 4;
   if ((st = upload(&P->d_adj, adj_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_adjm, adjm_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_pieces, pieces_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_rd, rd_all, P->device_bytes)) != MHT_OK) return st;
+  if ((st = upload(&P->d_rdtab, rdtab, P->device_bytes)) != MHT_OK) return st;
   return MHT_OK;
 }
 
@@ -678,6 +792,10 @@ Ctx make_ctx(mht_plan *P, int nrhs) {
   cx.part = P->d_part;
   cx.fsplit = P->d_fsplit;
   cx.fcount = P->d_fcount;
+  cx.rdtab = P->d_rdtab;
+  // fused group sums only at nrhs = 1: the multi-RHS gathers measured faster
+  // from the reduced workspace (profiles/r01_fused_sums_ab.txt)
+  cx.fused = (P->fused_sum && nrhs == 1) ? 1 : 0;
   cx.m = P->m;
   cx.n = P->n;
   cx.Zt = P->Zt;
@@ -745,8 +863,9 @@ mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
   };
   adj_stage(L + 1, true);
   for (int s = L; s >= 0; --s) {
-    timed(P, 2, s, nrhs, P->pieces[s].count, [&] {
-      launch_reduce(P->cplx, cx, P->d_pieces + P->pieces[s].off, P->d_rd, P->pieces[s].count, P->stream);
+    const Range pr = cx.fused ? P->pieces_u[s] : P->pieces[s];
+    timed(P, 2, s, nrhs, pr.count, [&] {
+      launch_reduce(P->cplx, cx, P->d_pieces + pr.off, P->d_rd, pr.count, P->stream);
     });
     adj_stage(s, false);
   }
@@ -829,7 +948,7 @@ mht_status mht_plan_info_get(const mht_plan *P, mht_plan_info *info) {
   int f = 0, a = 0;
   for (int s = 0; s < P->L + 2; ++s) {
     f += P->fwd[s].count > 0;
-    a += (P->adj[s].count > 0) + (s <= P->L && P->pieces[s].count > 0);
+    a += (P->adj[s].count > 0) + (s <= P->L && (P->fused_sum ? P->pieces_u[s] : P->pieces[s]).count > 0);
   }
   a += P->cpieces.count > 0;
   info->fwd_launches = f;
@@ -908,6 +1027,14 @@ mht_status mht_set_graphs(mht_plan *P, int on) {
   if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
   P->graphs = on != 0;
   if (!P->graphs) P->clear_graphs();
+  return MHT_OK;
+}
+
+mht_status mht_set_fused_sums(mht_plan *P, int on) {
+  if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  P->fused_sum = on != 0;
+  P->clear_graphs();
   return MHT_OK;
 }
 

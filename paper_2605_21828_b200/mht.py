@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(HERE, "libmht.so")
 MHT_DTYPE_F64, MHT_DTYPE_C128 = 1, 2
 EXPORTED = [
     "mht_plan_load", "mht_plan_info_get", "mht_plan_set_stream", "mht_reserve", "mht_apply",
-    "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host", "mht_set_graphs", "mht_sync",
+    "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host", "mht_set_graphs", "mht_set_fused_sums", "mht_sync",
     "mht_stage_stats", "mht_set_profiling", "mht_profile_get", "mht_profile_reset", "mht_plan_destroy",
     "mht_status_string", "mht_last_error", "mht_build_info",
 ]
@@ -59,6 +59,7 @@ def load_library(path: str = LIB_PATH):
     for nm in ("mht_apply", "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host"):
         getattr(L, nm).argtypes = [vp, vp, vp, i32]
     L.mht_set_graphs.argtypes = [vp, i32]
+    L.mht_set_fused_sums.argtypes = [vp, i32]
     L.mht_sync.argtypes = [vp]
     L.mht_stage_stats.argtypes = [vp, i32, C.POINTER(i64), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                   C.POINTER(C.c_int32)]
@@ -205,6 +206,14 @@ class Plan:
 
     def sync(self):
         _check(load_library().mht_sync(self._h), "mht_sync")
+
+    def set_graphs(self, on: bool):
+        _check(load_library().mht_set_graphs(self._h, int(bool(on))), "mht_set_graphs")
+
+    def set_fused_sums(self, on: bool):
+        """Adjoint group sums on the consumer's load (True, default) or as a
+        separate reduce pass per stage (False); bitwise identical results."""
+        _check(load_library().mht_set_fused_sums(self._h, int(bool(on))), "mht_set_fused_sums")
 
     def stage_stats(self):
         out = []

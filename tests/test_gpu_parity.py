@@ -237,3 +237,57 @@ def test_forward_split_k_low_parallelism(gpu, oracle_lib, plans):
     assert torch.equal(f1, f2)
     fd = torch.from_numpy(Phi).cuda() @ c[0]
     assert (torch.linalg.vector_norm(f1[0] - fd) / torch.linalg.vector_norm(fd)).item() < 1e-11
+
+
+def test_fused_group_sums_bitwise_equal_unfused(gpu, oracle_lib, plans):
+    """Adjoint group sums formed on the consumer's load (default) and by the
+    separate per-stage reduce pass give bitwise-identical results (same
+    partials, same order), on a plan with aliases/COPY blocks (tol ~ 0), a
+    compressed flat plan, and a real sphere plan; both match O2."""
+    cases = [flat_case(plans, 1024, 32, 4, 1e-15, name="exact"), flat_case(plans, 2048, 32, 4, 1e-8)]
+    lmax = 31
+    ws = W.sphere_workload(2048, lmax, 4, 1e-10)
+    sp = str(plans / "sph_fused.plan")
+    W.build_workload_plan(ws, sp, workers=8, log=None)
+    cases.append((sp, ws))
+    for path, w in cases:
+        P = gpu.Plan(path)
+        O = oracle_lib.Plan(path)
+        for nrhs in (1, 6, 32):
+            if w.dtype == "complex128":
+                y = mi.complex_gaussian(nrhs, w.n, 300 + nrhs)
+            else:
+                y = mi.real_gaussian(nrhs, w.n, 300 + nrhs)
+            yt = torch.from_numpy(y).cuda()
+            P.set_fused_sums(True)
+            a1 = P.adjoint(yt).cpu()
+            P.set_fused_sums(False)
+            a0 = P.adjoint(yt).cpu()
+            assert torch.equal(a1, a0), (path, nrhs)
+            assert rel_cols(a1.numpy(), O.adjoint(y)) <= PARITY
+        P.set_fused_sums(True)
+        P.close()
+
+
+def test_split_k_small_blocks(gpu, oracle_lib, plans):
+    """Few, short blocks (n_red 128..512) take the generalised split-column
+    forward path (>= 64 columns per split), and few, tall blocks (1000+ rows)
+    the split-row adjoint path (>= 128 rows per split), at nrhs = 1; parity vs
+    O2 and the dense product, and bitwise determinism of both directions."""
+    rng = np.random.default_rng(12)
+    for n, m, L in ((128, 1024, 1), (512, 768, 2), (192, 2048, 3), (4096, 256, 2), (3000, 200, 1)):
+        Phi = rng.standard_normal((n, m))
+        path = _dense_plan(plans, Phi, L, 1e-12, f"split_small_{n}_{m}_{L}")
+        w = mi.Workload("sks", "mesh", n, m, "float64", 1e-12, L)
+        P, _ = check_plan(gpu, oracle_lib, path, w, (1, 2))
+        c = torch.from_numpy(rng.standard_normal((1, m))).cuda()
+        f1, f2 = P.apply(c), P.apply(c)
+        assert torch.equal(f1, f2)
+        fd = torch.from_numpy(Phi).cuda() @ c[0]
+        assert (torch.linalg.vector_norm(f1[0] - fd) / torch.linalg.vector_norm(fd)).item() < 1e-11
+        y = torch.from_numpy(rng.standard_normal((1, n))).cuda()
+        a1, a2 = P.adjoint(y), P.adjoint(y)
+        assert torch.equal(a1, a2)
+        ad = torch.from_numpy(Phi).cuda().T @ y[0]
+        assert (torch.linalg.vector_norm(a1[0] - ad) / torch.linalg.vector_norm(ad)).item() < 1e-11
+        P.close()
