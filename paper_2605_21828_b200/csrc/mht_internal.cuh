@@ -42,8 +42,18 @@ struct DevBlock {
   int32_t pad2;     // adjoint row splits (nrhs = 1), 0 = none
   int64_t fsp_off;  // split scratch base of this block's forward row tiles (scalars)
   int64_t asp_off;  // split scratch base of this block's adjoint column tiles (scalars)
+  int32_t ld;       // leading dimension of T in the device pool (r_out, rounded up to
+                    // even for float64 so every column starts 16-byte aligned)
+  int32_t pad3;
 };
-static_assert(sizeof(DevBlock) == 128, "DevBlock layout");
+static_assert(sizeof(DevBlock) == 136, "DevBlock layout");
+
+// Device repack of one block's factor (real plans): column-major r_out x ncols
+// with ld = r_out  ->  ld = dst_ld (>= r_out), padding rows zero.
+struct Repack {
+  int64_t src_off, dst_off;
+  int32_t r_out, ncols, dst_ld, pad;
+};
 
 // A unit of work: rows [start, start+count) (forward) or redundant columns
 // [start, start+count) (adjoint) of block `blk`.
@@ -91,6 +101,20 @@ constexpr int ADJ_THREADS = 128;
 constexpr int ADJ_RCH = 256;     // adjoint rows staged in smem per pass
 constexpr int MMA_COLS = 64;     // redundant columns per multi-RHS adjoint tile
 
+// One phase of the persistent nrhs = 1 apply (a stage's tiles or a list of
+// group-sum pieces), separated from the next by a grid barrier.
+enum : int32_t { PH_FWD = 0, PH_ADJ = 1, PH_SUM = 2 };
+struct Phase {
+  int32_t kind;    // PH_FWD | PH_ADJ | PH_SUM
+  int32_t from_f;  // PH_ADJ: input is f through perm_x (leaf stage)
+  int32_t off;     // first tile / piece
+  int32_t count;   // tiles / pieces
+  int32_t stage;   // plan stage (-1: the sums into c)
+  int32_t pad;
+};
+constexpr int PERSIST_THREADS = 128;
+
+
 // Launchers (mht_kernels.cu).  is_complex selects double2 vs double.
 void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, void *stream);
 void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
@@ -99,6 +123,12 @@ void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, 
 // adjoint uses 64-column tiles (adjm lists).
 void launch_mma(bool is_complex, bool adjoint, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
                 void *stream);
+// persistent apply: returns a cudaError_t value (0 = launched)
+int launch_persist(bool is_complex, const Ctx &ctx, const Phase *phases, int nph, const Tile *ftiles,
+                   const Tile *atiles, const Piece *pieces, const int64_t *rd, int *ctr, unsigned long long *stamps,
+                   int grid, void *stream);
+int persist_grid(bool is_complex);
+void launch_repack(const double *src, double *dst, const Repack *jobs, int njobs, void *stream);
 void launch_reduce(bool is_complex, const Ctx &ctx, const Piece *pieces, const int64_t *rd,
                    int npieces, void *stream);
 

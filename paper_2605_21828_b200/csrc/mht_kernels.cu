@@ -13,10 +13,14 @@
 // registers.
 #include <cuda_runtime.h>
 
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 #include <cstring>
 
 #include "mht_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace mht {
 namespace {
@@ -40,6 +44,12 @@ struct Tr<double> {
   static __device__ __forceinline__ double ldT(const double *p) {
     double v;
     asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+  }
+  // two consecutive rows of a (16-byte aligned) real factor column
+  static __device__ __forceinline__ double2 ldT2(const double *p) {
+    double2 v;
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
     return v;
   }
 };
@@ -79,13 +89,19 @@ struct Tr<double2> {
 };
 
 // in[q] for right-hand side r: two segments, each in c (ld m) or zpool (ld Zt).
-template <class S>
+// CG: read the workspace through L2 only (ld.global.cg).  The persistent
+// kernel writes and reads workspace in different phases of ONE launch, and L1
+// is not coherent: a line cached while reading one stage's z could be stale
+// for the next stage's entries that share it.
+template <class S, bool CG = false>
 __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, int r) {
   const bool s1 = q >= B.seg_len[0];  // no dynamic indexing: keeps B in registers
   const int64_t off = s1 ? B.seg_off[1] + (q - B.seg_len[0]) : B.seg_off[0] + q;
   const int32_t src = s1 ? B.seg_src[1] : B.seg_src[0];
   if (src == SRC_C) return static_cast<const S *>(cx.c)[r * cx.m + off];  // user layout: column-major
-  return static_cast<const S *>(cx.z)[off * cx.nrhs + r];                   // workspace: RHS-fastest
+  const S *p = static_cast<const S *>(cx.z) + off * cx.nrhs + r;           // workspace: RHS-fastest
+  if constexpr (CG) return Tr<S>::ldcg(p);
+  return *p;
 }
 
 // ------------------------------------------------------------------------
@@ -97,9 +113,8 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
 // adds them in split order — deterministic, no float atomics.
 // ------------------------------------------------------------------------
 template <class S>
-__global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Tile *__restrict__ tiles) {
+__device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
   using X = Tr<S>;
-  const Tile tl = tiles[blockIdx.y];
   const DevBlock B = cx.blocks[tl.blk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ra = tl.start + lane, rb = tl.start + 32 + lane;
@@ -114,39 +129,52 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Ti
   }
   S acc_a = X::zero(), acc_b = X::zero();
   const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
-  const int64_t ld = B.r_out;
+  const int64_t ld = B.ld;
+  // complex: lane owns rows l and l + 32 (one 16-byte load each); real: lane
+  // owns the row pair 2l, 2l + 1 (one 16-byte load; columns are 16-byte
+  // aligned by the loader's repack, the pad row is zero)
+  constexpr bool REAL = sizeof(S) == 8;
+  const bool vp = 2 * lane < tl.count;
   for (int j0 = jbeg + warp * 32; j0 < jend; j0 += FWD_THREADS) {
     const int j = j0 + lane;
     S xr = X::zero();
     if (j < jend) {
       const int q = (B.flags & F_RED_IOTA) ? j : cx.idx[B.red_off + j];
-      xr = in_value<S>(cx, B, q, 0);
+      xr = in_value<S, true>(cx, B, q, 0);
     }
     const int jn = min(32, jend - j0);
     const S *col = T + (int64_t)j0 * ld;
+    auto step = [&](int jj) {
+      const S x = X::shfl(xr, jj);
+      if constexpr (REAL) {
+        // predicated load (not a branch) so the unrolled loads are all in flight
+        const double2 t = vp ? Tr<double>::ldT2(reinterpret_cast<const double *>(col) + (int64_t)jj * ld + tl.start + 2 * lane)
+                             : make_double2(0.0, 0.0);
+        X::fma(acc_a, t.x, x);
+        X::fma(acc_b, t.y, x);
+      } else {
+        const S ta = va ? X::ldT(col + (int64_t)jj * ld + ra) : X::zero();
+        const S tb = vb ? X::ldT(col + (int64_t)jj * ld + rb) : X::zero();
+        X::fma(acc_a, ta, x);
+        X::fma(acc_b, tb, x);
+      }
+    };
     if (jn == 32) {
 #pragma unroll 8
-      for (int jj = 0; jj < 32; ++jj) {
-        const S ta = va ? X::ldT(col + (int64_t)jj * ld + ra) : X::zero();
-        const S tb = vb ? X::ldT(col + (int64_t)jj * ld + rb) : X::zero();
-        const S x = X::shfl(xr, jj);
-        X::fma(acc_a, ta, x);
-        X::fma(acc_b, tb, x);
-      }
+      for (int jj = 0; jj < 32; ++jj) step(jj);
     } else {
-      for (int jj = 0; jj < jn; ++jj) {
-        const S ta = va ? X::ldT(col + (int64_t)jj * ld + ra) : X::zero();
-        const S tb = vb ? X::ldT(col + (int64_t)jj * ld + rb) : X::zero();
-        const S x = X::shfl(xr, jj);
-        X::fma(acc_a, ta, x);
-        X::fma(acc_b, tb, x);
-      }
+      for (int jj = 0; jj < jn; ++jj) step(jj);
     }
   }
   __shared__ S red[FWD_THREADS / 32][FWD_ROWS];
   __shared__ int last;
-  red[warp][lane] = acc_a;
-  red[warp][lane + 32] = acc_b;
+  if constexpr (REAL) {
+    red[warp][2 * lane] = acc_a;
+    red[warp][2 * lane + 1] = acc_b;
+  } else {
+    red[warp][lane] = acc_a;
+    red[warp][lane + 32] = acc_b;
+  }
   __syncthreads();
   S *scratch = static_cast<S *>(cx.fsplit);
   const int grp = tl.pad >> 8;
@@ -181,7 +209,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Ti
     const int row = tl.start + i;
     if (row < B.n_skel) {
       const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
-      s = X::add(s, in_value<S>(cx, B, q, 0));
+      s = X::add(s, in_value<S, true>(cx, B, q, 0));
     }
     if (B.flags & F_OUT_F)
       static_cast<S *>(cx.fout)[cx.perm[B.out_off + row]] = s;
@@ -191,22 +219,32 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Ti
   if (split && threadIdx.x == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
 }
 
+template <class S>
+__global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Tile *__restrict__ tiles) {
+  fwd_tile<S>(cx, tiles[blockIdx.y]);
+}
+
 // adjoint input z[i] of a block: f through perm_x (leaf stage), else the group
 // sum of its readers' partials (the adjoint of a block row that
 // feeds two transfers is the sum of both), either summed here on load (fused:
 // no separate reduction pass) or read from the zpool slot reduce_kernel wrote.
 // The fused sum adds the partials in the same (reader id) order as
 // reduce_kernel, so both paths are bitwise identical.
-template <class S>
+template <class S, bool CG = false>
 __device__ __forceinline__ S adj_in(const Ctx &cx, const DevBlock &B, int i, int r, bool from_f) {
   if (from_f) return static_cast<const S *>(cx.fin)[r * cx.n + cx.perm[B.out_off + i]];
   if (cx.fused && B.rd_cnt >= 0) {
     const S *part = static_cast<const S *>(cx.part);
     S s = Tr<S>::zero();
-    for (int k = 0; k < B.rd_cnt; ++k) s = Tr<S>::add(s, part[(cx.rdtab[B.rd_off + k] + i) * cx.nrhs + r]);
+    for (int k = 0; k < B.rd_cnt; ++k) {
+      const S *p = part + (cx.rdtab[B.rd_off + k] + i) * cx.nrhs + r;
+      s = Tr<S>::add(s, CG ? Tr<S>::ldcg(p) : *p);
+    }
     return s;
   }
-  return static_cast<const S *>(cx.z)[(B.out_off + i) * cx.nrhs + r];
+  const S *p = static_cast<const S *>(cx.z) + (B.out_off + i) * cx.nrhs + r;
+  if constexpr (CG) return Tr<S>::ldcg(p);
+  return *p;
 }
 
 // ------------------------------------------------------------------------
@@ -220,15 +258,12 @@ __device__ __forceinline__ S adj_in(const Ctx &cx, const DevBlock &B, int i, int
 // them in split order (deterministic, no float atomics).
 // ------------------------------------------------------------------------
 template <class S, int RB>
-__global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Tile *__restrict__ tiles,
-                                                         int from_f) {
+__device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_f, int rhs0) {
   using X = Tr<S>;
-  // columns per warp: 8 complex / 16 real (same 128 bytes in flight per lane per row step)
+  // columns per warp: 8 complex / 16 real
   constexpr int ACOLS = adj_cols<S>();
   constexpr int CPW = ACOLS / (ADJ_THREADS / 32);
-  const Tile tl = tiles[blockIdx.y];
   const DevBlock B = cx.blocks[tl.blk];
-  const int rhs0 = blockIdx.x * RB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool split = tl.pad >= 0;
   const int sidx = split ? (tl.pad & 255) : 0;
@@ -246,18 +281,38 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Ti
 #pragma unroll
     for (int k = 0; k < RB; ++k) acc[u][k] = X::zero();
   const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
-  const int64_t ld = B.r_out;
+  const int64_t ld = B.ld;
   const int cbase = tl.start + warp * CPW;
   const int cend = tl.start + tl.count;
+  constexpr bool REAL = sizeof(S) == 8;
 
   for (int rc = rbeg; rc < rend; rc += ADJ_RCH) {
     const int rn = min(ADJ_RCH, rend - rc);
     for (int e = threadIdx.x; e < rn * RB; e += ADJ_THREADS) {
       const int i = e % rn, k = e / rn;
-      zs[i][k] = (rhs0 + k < cx.nrhs) ? adj_in<S>(cx, B, rc + i, rhs0 + k, from_f) : X::zero();
+      zs[i][k] = (rhs0 + k < cx.nrhs) ? adj_in<S, true>(cx, B, rc + i, rhs0 + k, from_f) : X::zero();
     }
+    if (REAL && (rn & 1) && threadIdx.x < RB) zs[rn][threadIdx.x] = X::zero();  // pair partner of the last row
     __syncthreads();
-    if (cbase < cend) {
+    if constexpr (REAL) {
+      // real: lane takes the row pair (2q, 2q + 1) of each of its columns with
+      // one 16-byte load (rc is even; the pad row of an odd r_out is zero)
+      static_assert(!REAL || RB == 1, "real pair path is the nrhs = 1 kernel");
+      if (cbase < cend) {
+        for (int q = lane; 2 * q < rn; q += 32) {
+          const double z0 = zs[2 * q][0], z1 = zs[2 * q + 1][0];
+#pragma unroll
+          for (int u = 0; u < CPW; ++u) {
+            if (cbase + u < cend) {
+              const double2 t = Tr<double>::ldT2(reinterpret_cast<const double *>(T) + (int64_t)(cbase + u) * ld + rc + 2 * q);
+              double &a = reinterpret_cast<double &>(acc[u][0]);
+              a = ::fma(t.x, z0, a);
+              a = ::fma(t.y, z1, a);
+            }
+          }
+        }
+      }
+    } else if (cbase < cend) {
       for (int i = lane; i < rn; i += 32) {
         S zv[RB];
 #pragma unroll
@@ -280,7 +335,7 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Ti
       const int i = e % B.n_skel, k = e / B.n_skel;
       if (rhs0 + k >= cx.nrhs) continue;
       const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
-      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0 + k] = adj_in<S>(cx, B, i, rhs0 + k, from_f);
+      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0 + k] = adj_in<S, true>(cx, B, i, rhs0 + k, from_f);
     }
   }
   // warp reductions
@@ -328,6 +383,12 @@ __global__ void __launch_bounds__(ADJ_THREADS) adj_kernel(const Ctx cx, const Ti
     }
     if (threadIdx.x == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
   }
+}
+
+template <class S, int RB>
+__global__ void __launch_bounds__(ADJ_THREADS, 7) adj_kernel(const Ctx cx, const Tile *__restrict__ tiles,
+                                                             int from_f) {
+  adj_tile<S, RB>(cx, tiles[blockIdx.y], from_f, blockIdx.x * RB);
 }
 
 // ------------------------------------------------------------------------
@@ -411,7 +472,7 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
-  const int64_t ld = B.r_out;
+  const int64_t ld = B.ld;
   const int K = ADJ ? B.r_out : B.n_red;
   const int nchunks = (K + BK - 1) / BK;
   const bool red_iota = (B.flags & F_RED_IOTA) != 0;
@@ -612,23 +673,82 @@ void mma_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cuda
 // adjoint group sums: dst = sum of the readers' partial ranges (fixed order,
 // no atomics).
 // ------------------------------------------------------------------------
-template <class S>
-__global__ void __launch_bounds__(256) reduce_kernel(const Ctx cx, const Piece *__restrict__ pieces,
-                                                     const int64_t *__restrict__ rd) {
+template <class S, bool CG>
+__device__ __forceinline__ void reduce_piece(const Ctx &cx, const Piece p, const int64_t *__restrict__ rd,
+                                             int slice = 0, int nslices = 1) {
   using X = Tr<S>;
-  const Piece p = pieces[blockIdx.x];
   const S *part = static_cast<const S *>(cx.part);
   const int nr = cx.nrhs;
   const int total = p.len * nr;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+  for (int e = slice * blockDim.x + threadIdx.x; e < total; e += nslices * blockDim.x) {
     const int i = e / nr, r = e - (e / nr) * nr;  // RHS fastest (workspace layout)
     S s = X::zero();
-    for (int q = 0; q < p.rd_count; ++q) s = X::add(s, part[(rd[p.rd_begin + q] + i) * nr + r]);
+    for (int q = 0; q < p.rd_count; ++q) {
+      const S *a = part + (rd[p.rd_begin + q] + i) * nr + r;
+      s = X::add(s, CG ? X::ldcg(a) : *a);
+    }
     if (p.dst_src == SRC_C)
       static_cast<S *>(cx.cw)[r * cx.m + p.dst_off + i] = s;
     else
       static_cast<S *>(cx.z)[(p.dst_off + i) * nr + r] = s;
   }
+}
+
+template <class S>
+__global__ void __launch_bounds__(256) reduce_kernel(const Ctx cx, const Piece *__restrict__ pieces,
+                                                     const int64_t *__restrict__ rd) {
+  reduce_piece<S, false>(cx, pieces[blockIdx.x], rd, blockIdx.y, gridDim.y);  // y: slices of wide pieces
+}
+
+// ------------------------------------------------------------------------
+// persistent nrhs = 1 apply: ONE cooperative launch walks all phases of a
+// direction (forward: stages 0..L+1; adjoint: leaf stage, then per stage the
+// unfused group sums and the stage, then the sums into c).  CTAs pull tiles
+// from a per-phase atomic counter (largest first: the tile lists are LPT
+// sorted) and meet at a grid barrier between phases, so a small plan pays one
+// launch instead of L+2 and no per-stage ramp/drain.  The phase bodies are
+// the same tile functions the per-stage kernels run.
+// ------------------------------------------------------------------------
+template <class S, int MINB>
+__global__ void __launch_bounds__(PERSIST_THREADS, MINB) persist_kernel(const Ctx cx, const Phase *__restrict__ phases,
+                                                                 int nph, const Tile *__restrict__ ftiles,
+                                                                 const Tile *__restrict__ atiles,
+                                                                 const Piece *__restrict__ pieces,
+                                                                 const int64_t *__restrict__ rd, int *ctr,
+                                                                 unsigned long long *stamps) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ int t_sh;
+  if (stamps && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    stamps[0] = ns;
+  }
+  for (int p = 0; p < nph; ++p) {
+    const Phase ph = phases[p];
+    for (;;) {
+      if (threadIdx.x == 0) t_sh = atomicAdd(ctr + p, 1);
+      __syncthreads();
+      const int t = t_sh;
+      __syncthreads();
+      if (t >= ph.count) break;
+      if (ph.kind == PH_FWD)
+        fwd_tile<S>(cx, ftiles[ph.off + t]);
+      else if (ph.kind == PH_ADJ)
+        adj_tile<S, 1>(cx, atiles[ph.off + t], ph.from_f, 0);
+      else
+        reduce_piece<S, true>(cx, pieces[ph.off + t], rd);
+      __syncthreads();
+    }
+    grid.sync();
+    if (stamps && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long ns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+      stamps[p + 1] = ns;
+    }
+  }
+  // every CTA is past its last atomicAdd: re-arm the counters for the next apply
+  if (blockIdx.x == 0)
+    for (int p = threadIdx.x; p < nph; p += blockDim.x) ctr[p] = 0;
 }
 
 constexpr int MAX_GRID_Y = 65535;
@@ -682,13 +802,89 @@ void launch_mma(bool is_complex, bool adjoint, const Ctx &ctx, const Tile *tiles
   }
 }
 
+namespace {
+__global__ void __launch_bounds__(256) repack_kernel(const double *__restrict__ src, double *__restrict__ dst,
+                                                     const Repack *__restrict__ jobs) {
+  const Repack J = jobs[blockIdx.x];
+  const int64_t total = (int64_t)J.dst_ld * J.ncols;
+  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+    const int64_t j = e / J.dst_ld;
+    const int i = (int)(e - j * J.dst_ld);
+    dst[J.dst_off + e] = i < J.r_out ? src[J.src_off + j * J.r_out + i] : 0.0;
+  }
+}
+}  // namespace
+
+void launch_repack(const double *src, double *dst, const Repack *jobs, int njobs, void *stream) {
+  for (int j0 = 0; j0 < njobs; j0 += 65535) {
+    const int nj = njobs - j0 < 65535 ? njobs - j0 : 65535;
+    repack_kernel<<<nj, 256, 0, (cudaStream_t)stream>>>(src, dst, jobs + j0);
+  }
+}
+
+// MINB = CTAs per SM the register budget is sized for: 5 (96 registers; the
+// complex body spills ~200 B outside its loops) or 4 (128, no spills).
+// MHT_PERSIST_MINB=4|5 selects (default 5).
+inline int persist_minb() {
+  static int v = [] {
+    const char *e = getenv("MHT_PERSIST_MINB");
+    return (e && atoi(e) == 4) ? 4 : 5;
+  }();
+  return v;
+}
+
+template <class S, int MINB>
+cudaError_t persist_launch(const Ctx &ctx, const Phase *phases, int nph, const Tile *ftiles, const Tile *atiles,
+                           const Piece *pieces, const int64_t *rd, int *ctr, unsigned long long *stamps, int grid,
+                           cudaStream_t st) {
+  Ctx c = ctx;
+  void *args[] = {(void *)&c, (void *)&phases, (void *)&nph, (void *)&ftiles, (void *)&atiles, (void *)&pieces,
+                  (void *)&rd, (void *)&ctr, (void *)&stamps};
+  return cudaLaunchCooperativeKernel((const void *)persist_kernel<S, MINB>, dim3(grid), dim3(PERSIST_THREADS), args, 0,
+                                     st);
+}
+
+template <class S>
+int persist_grid_t() {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (persist_minb() == 4)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, persist_kernel<S, 4>, PERSIST_THREADS, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, persist_kernel<S, 5>, PERSIST_THREADS, 0);
+  return sms * per;
+}
+
+int persist_grid(bool is_complex) { return is_complex ? persist_grid_t<double2>() : persist_grid_t<double>(); }
+
+template <class S>
+cudaError_t persist_dispatch(const Ctx &ctx, const Phase *phases, int nph, const Tile *ftiles, const Tile *atiles,
+                             const Piece *pieces, const int64_t *rd, int *ctr, unsigned long long *stamps, int grid,
+                             cudaStream_t st) {
+  if (persist_minb() == 4) return persist_launch<S, 4>(ctx, phases, nph, ftiles, atiles, pieces, rd, ctr, stamps, grid, st);
+  return persist_launch<S, 5>(ctx, phases, nph, ftiles, atiles, pieces, rd, ctr, stamps, grid, st);
+}
+
+int launch_persist(bool is_complex, const Ctx &ctx, const Phase *phases, int nph, const Tile *ftiles,
+                   const Tile *atiles, const Piece *pieces, const int64_t *rd, int *ctr, unsigned long long *stamps,
+                   int grid, void *stream) {
+  if (nph <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = is_complex ? persist_dispatch<double2>(ctx, phases, nph, ftiles, atiles, pieces, rd, ctr, stamps, grid, st)
+                             : persist_dispatch<double>(ctx, phases, nph, ftiles, atiles, pieces, rd, ctr, stamps, grid, st);
+  return (int)e;
+}
+
 void launch_reduce(bool is_complex, const Ctx &ctx, const Piece *pieces, const int64_t *rd,
                    int npieces, void *stream) {
   if (npieces <= 0) return;
+  // a piece is <= 1024 entries x nrhs values: give every 2048 values a CTA
+  const int ny = ctx.nrhs <= 2 ? 1 : (ctx.nrhs / 2 < 64 ? ctx.nrhs / 2 : 64);
   if (is_complex)
-    reduce_kernel<double2><<<npieces, 256, 0, (cudaStream_t)stream>>>(ctx, pieces, rd);
+    reduce_kernel<double2><<<dim3(npieces, ny), 256, 0, (cudaStream_t)stream>>>(ctx, pieces, rd);
   else
-    reduce_kernel<double><<<npieces, 256, 0, (cudaStream_t)stream>>>(ctx, pieces, rd);
+    reduce_kernel<double><<<dim3(npieces, ny), 256, 0, (cudaStream_t)stream>>>(ctx, pieces, rd);
 }
 
 }  // namespace mht

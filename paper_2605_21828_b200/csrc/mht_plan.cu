@@ -104,6 +104,19 @@ struct mht_plan {
 
   std::vector<Range> fwd, fwd1, adj, adjm, pieces;  // per stage 0..L+1
   std::vector<Range> pieces_u;  // pieces of the producers that are not fused (fused mode)
+  // persistent nrhs = 1 apply (one cooperative launch per direction)
+  // off by default: with CUDA-graph replay the per-stage launches measured
+  // faster (profiles/r01_persistent_ab.txt: the cooperative kernel's union
+  // body needs 96-128 registers, 4-5 CTAs/SM, against 7 for the adjoint alone)
+  int persist = 0;              // 1 on (one cooperative launch per direction), 0 per-stage launches
+  int persist_grid = 0;
+  Phase *d_phases = nullptr;
+  Range ph_fwd, ph_adj_fused, ph_adj_unfused;
+  std::vector<Phase> h_phases;
+  int *d_ctr = nullptr;
+  unsigned long long *d_stamps = nullptr;  // per-phase globaltimer stamps (profiling)
+  std::vector<double> last_phase_ms[2];    // [dir] per-phase durations of the last profiled apply
+  bool want_stamps[2] = {false, false};
   int64_t *d_rdtab = nullptr;
   bool fused_sum = true;        // adjoint group sums on the consumer's load (MHT_FUSED_SUM=0: off)
   int n_unfused = 0;
@@ -134,7 +147,7 @@ struct mht_plan {
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd, (void *)d_fwd1, d_fsplit, (void *)d_fcount,
-                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, d_z, d_part, d_hc, d_hf})
+                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, (void *)d_phases, (void *)d_ctr, (void *)d_stamps, d_z, d_part, d_hc, d_hf})
       if (p) cudaFree(p);
   }
 };
@@ -450,6 +463,49 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
   P->Pt = std::max<int64_t>(Pp, 1);
   P->n_mat = (int)blocks.size();
 
+  // ------------------------------------------------ factor layout
+  // Complex factors keep the file layout (16-byte scalars are always aligned).
+  // Real factors are repacked on the device so every column of every block
+  // starts 16-byte aligned (ld rounded up to even, zero pad row): the nrhs = 1
+  // kernels then stream two rows per 16-byte load.
+  for (DevBlock &D : blocks) D.ld = D.r_out;
+  if (!P->cplx && coef_cursor > 0) {
+    std::vector<Repack> jobs;
+    int64_t cur = 0;
+    for (DevBlock &D : blocks) {
+      if (D.n_red == 0 || D.r_out == 0) continue;  // COPY / empty: no coefficients
+      Repack J;
+      memset(&J, 0, sizeof J);
+      J.src_off = D.coef_off;
+      J.dst_off = cur;
+      J.r_out = D.r_out;
+      J.ncols = D.n_red;
+      J.dst_ld = D.r_out + (D.r_out & 1);
+      D.coef_off = cur;
+      D.ld = J.dst_ld;
+      cur += (int64_t)J.dst_ld * J.ncols;
+      cur += cur & 1;
+      jobs.push_back(J);
+    }
+    void *np = nullptr;
+    const size_t nbytes = (size_t)std::max<int64_t>(cur + 2, 16) * sizeof(double);  // +2: pair loads past the end
+    CUDA_TRY(cudaMalloc(&np, nbytes));
+    CUDA_TRY(cudaMemsetAsync(np, 0, nbytes, P->stream));
+    Repack *dj = nullptr;
+    CUDA_TRY(cudaMalloc((void **)&dj, std::max<size_t>(1, jobs.size()) * sizeof(Repack)));
+    if (!jobs.empty()) {
+      CUDA_TRY(cudaMemcpy(dj, jobs.data(), jobs.size() * sizeof(Repack), cudaMemcpyHostToDevice));
+      launch_repack(static_cast<const double *>(P->d_coef), static_cast<double *>(np), dj, (int)jobs.size(), P->stream);
+    }
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    cudaFree(dj);
+    cudaFree(P->d_coef);
+    P->device_bytes -= (int64_t)pool_bytes;
+    P->d_coef = np;
+    P->device_bytes += (int64_t)nbytes;
+  }
+
   // ------------------------------------------------ tiles (LPT order per stage)
   std::vector<std::vector<std::pair<int64_t, Tile>>> ft(L + 2), at(L + 2), amt(L + 2);
   for (int i = 0; i < (int)blocks.size(); ++i) {
@@ -742,6 +798,36 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
   }
   if (const char *e = getenv("MHT_FUSED_SUM")) P->fused_sum = strcmp(e, "0") != 0;
 
+  // ------------------------------------------------ persistent phases (nrhs = 1)
+  {
+    auto add = [&](int32_t kind, int32_t from_f, Range r, int32_t stage) {
+      if (r.count <= 0) return;
+      Phase ph;
+      memset(&ph, 0, sizeof ph);
+      ph.kind = kind;
+      ph.from_f = from_f;
+      ph.off = r.off;
+      ph.count = r.count;
+      ph.stage = stage;
+      P->h_phases.push_back(ph);
+    };
+    P->ph_fwd.off = (int32_t)P->h_phases.size();
+    for (int s = 0; s < L + 2; ++s) add(PH_FWD, 0, P->fwd1[s], s);
+    P->ph_fwd.count = (int32_t)P->h_phases.size() - P->ph_fwd.off;
+    for (int fused = 1; fused >= 0; --fused) {
+      Range &R = fused ? P->ph_adj_fused : P->ph_adj_unfused;
+      R.off = (int32_t)P->h_phases.size();
+      add(PH_ADJ, 1, P->adj[L + 1], L + 1);
+      for (int s = L; s >= 0; --s) {
+        add(PH_SUM, 0, fused ? P->pieces_u[s] : P->pieces[s], s);
+        add(PH_ADJ, 0, P->adj[s], s);
+      }
+      add(PH_SUM, 0, P->cpieces, -1);
+      R.count = (int32_t)P->h_phases.size() - R.off;
+    }
+  }
+  if (const char *e = getenv("MHT_PERSIST")) P->persist = atoi(e) != 0 ? 1 : 0;
+
   // ------------------------------------------------ upload
   mht_status st;
   if ((st = upload(&P->d_idx, idx_all, P->device_bytes)) != MHT_OK) return st;
@@ -764,6 +850,16 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
   if ((st = upload(&P->d_pieces, pieces_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_rd, rd_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_rdtab, rdtab, P->device_bytes)) != MHT_OK) return st;
+  if ((st = upload(&P->d_phases, P->h_phases, P->device_bytes)) != MHT_OK) return st;
+  {
+    const int maxph = std::max<int>(1, std::max(P->ph_fwd.count, std::max(P->ph_adj_fused.count, P->ph_adj_unfused.count)));
+    CUDA_TRY(cudaMalloc((void **)&P->d_ctr, (size_t)maxph * sizeof(int)));
+    CUDA_TRY(cudaMemset(P->d_ctr, 0, (size_t)maxph * sizeof(int)));
+    CUDA_TRY(cudaMalloc((void **)&P->d_stamps, (size_t)(maxph + 1) * 2 * sizeof(unsigned long long)));
+    P->device_bytes += (int64_t)maxph * 4 + (maxph + 1) * 16;
+  }
+  P->persist_grid = persist_grid(P->cplx);
+  if (P->persist_grid <= 0) P->persist = 0;
   return MHT_OK;
 }
 
@@ -832,10 +928,35 @@ void timed(mht_plan *P, int kind, int stage, int nrhs, int count, F &&launch) {
   P->recs.push_back({kind, stage, nrhs, a, b});
 }
 
+bool use_persist(const mht_plan *P, int nrhs) { return nrhs == 1 && P->persist != 0; }
+
+unsigned long long *stamp_buf(mht_plan *P, int dir) {
+  if (!P->prof) return nullptr;
+  P->want_stamps[dir] = true;
+  const int maxph = std::max<int>(1, std::max(P->ph_fwd.count, std::max(P->ph_adj_fused.count, P->ph_adj_unfused.count)));
+  return P->d_stamps + dir * (maxph + 1);
+}
+
+mht_status run_persist(mht_plan *P, const Ctx &cx, Range ph, int dir) {
+  int err = 0;
+  timed(P, dir, -2, 1, 1, [&] {
+    err = launch_persist(P->cplx, cx, P->d_phases + ph.off, ph.count, P->d_fwd1, P->d_adj, P->d_pieces, P->d_rd,
+                         P->d_ctr, stamp_buf(P, dir), P->persist_grid, P->stream);
+  });
+  if (err != 0) return fail(MHT_ERR_CUDA, std::string("persistent launch: ") + cudaGetErrorString((cudaError_t)err));
+  return MHT_OK;
+}
+
 mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs) {
   Ctx cx = make_ctx(P, nrhs);
   cx.c = c;
   cx.fout = f;
+  if (use_persist(P, nrhs)) {
+    mht_status st = run_persist(P, cx, P->ph_fwd, 0);
+    if (st != MHT_OK) return st;
+    CUDA_TRY(cudaGetLastError());
+    return MHT_OK;
+  }
   for (int s = 0; s < P->L + 2; ++s)
     timed(P, 0, s, nrhs, nrhs == 1 ? P->fwd1[s].count : P->fwd[s].count, [&] {
       if (nrhs == 1)
@@ -852,6 +973,12 @@ mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
   cx.fin = f;
   cx.cw = c;
   const int L = P->L;
+  if (use_persist(P, nrhs)) {
+    mht_status st = run_persist(P, cx, cx.fused ? P->ph_adj_fused : P->ph_adj_unfused, 1);
+    if (st != MHT_OK) return st;
+    CUDA_TRY(cudaGetLastError());
+    return MHT_OK;
+  }
   auto adj_stage = [&](int s, bool from_f) {
     if (nrhs == 1)
       timed(P, 1, s, nrhs, P->adj[s].count,
@@ -1035,6 +1162,33 @@ mht_status mht_set_fused_sums(mht_plan *P, int on) {
   CUDA_TRY(cudaStreamSynchronize(P->stream));
   P->fused_sum = on != 0;
   P->clear_graphs();
+  return MHT_OK;
+}
+
+mht_status mht_set_persistent(mht_plan *P, int on) {
+  if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  P->persist = (on != 0 && P->persist_grid > 0) ? 1 : 0;
+  P->clear_graphs();
+  return MHT_OK;
+}
+
+mht_status mht_phase_times(mht_plan *P, int dir, double *ms, int32_t *stage, int32_t *kind, int cap, int *nphases) {
+  if (!P || !nphases || dir < 0 || dir > 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  *nphases = 0;
+  if (!P->want_stamps[dir]) return MHT_OK;
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  const Range ph = dir == 0 ? P->ph_fwd : (P->fused_sum ? P->ph_adj_fused : P->ph_adj_unfused);
+  const int maxph = std::max<int>(1, std::max(P->ph_fwd.count, std::max(P->ph_adj_fused.count, P->ph_adj_unfused.count)));
+  std::vector<unsigned long long> st(ph.count + 1);
+  CUDA_TRY(cudaMemcpy(st.data(), P->d_stamps + dir * (maxph + 1), st.size() * 8, cudaMemcpyDeviceToHost));
+  const int n = std::min(cap, ph.count);
+  for (int i = 0; i < n; ++i) {
+    if (ms) ms[i] = (double)(st[i + 1] - st[i]) * 1e-6;
+    if (stage) stage[i] = P->h_phases[ph.off + i].stage;
+    if (kind) kind[i] = P->h_phases[ph.off + i].kind;
+  }
+  *nphases = n;
   return MHT_OK;
 }
 

@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(HERE, "libmht.so")
 MHT_DTYPE_F64, MHT_DTYPE_C128 = 1, 2
 EXPORTED = [
     "mht_plan_load", "mht_plan_info_get", "mht_plan_set_stream", "mht_reserve", "mht_apply",
-    "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host", "mht_set_graphs", "mht_set_fused_sums", "mht_sync",
+    "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host", "mht_set_graphs", "mht_set_fused_sums", "mht_set_persistent", "mht_phase_times", "mht_sync",
     "mht_stage_stats", "mht_set_profiling", "mht_profile_get", "mht_profile_reset", "mht_plan_destroy",
     "mht_status_string", "mht_last_error", "mht_build_info",
 ]
@@ -60,6 +60,9 @@ def load_library(path: str = LIB_PATH):
         getattr(L, nm).argtypes = [vp, vp, vp, i32]
     L.mht_set_graphs.argtypes = [vp, i32]
     L.mht_set_fused_sums.argtypes = [vp, i32]
+    L.mht_set_persistent.argtypes = [vp, i32]
+    L.mht_phase_times.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int32), C.POINTER(C.c_int32), i32,
+                                  C.POINTER(C.c_int32)]
     L.mht_sync.argtypes = [vp]
     L.mht_stage_stats.argtypes = [vp, i32, C.POINTER(i64), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                   C.POINTER(C.c_int32)]
@@ -209,6 +212,22 @@ class Plan:
 
     def set_graphs(self, on: bool):
         _check(load_library().mht_set_graphs(self._h, int(bool(on))), "mht_set_graphs")
+
+    def set_persistent(self, on: bool):
+        """nrhs = 1 applies as one cooperative launch per direction (True) or
+        one launch per stage (False, default); bitwise identical results."""
+        _check(load_library().mht_set_persistent(self._h, int(bool(on))), "mht_set_persistent")
+
+    def phase_times(self, direction: int):
+        """[(stage, kind, ms)] of the last profiled persistent apply (kind 0
+        forward stage, 1 adjoint stage, 2 group sums; stage -1 = sums into c)."""
+        cap = 4 * (self.L + 3)
+        ms = (C.c_double * cap)()
+        st = (C.c_int32 * cap)()
+        kd = (C.c_int32 * cap)()
+        n = C.c_int32()
+        _check(load_library().mht_phase_times(self._h, direction, ms, st, kd, cap, C.byref(n)), "mht_phase_times")
+        return [(st[i], kd[i], ms[i]) for i in range(n.value)]
 
     def set_fused_sums(self, on: bool):
         """Adjoint group sums on the consumer's load (True, default) or as a

@@ -275,7 +275,7 @@ def test_split_k_small_blocks(gpu, oracle_lib, plans):
     the split-row adjoint path (>= 128 rows per split), at nrhs = 1; parity vs
     O2 and the dense product, and bitwise determinism of both directions."""
     rng = np.random.default_rng(12)
-    for n, m, L in ((128, 1024, 1), (512, 768, 2), (192, 2048, 3), (4096, 256, 2), (3000, 200, 1)):
+    for n, m, L in ((128, 1024, 1), (512, 768, 2), (192, 2048, 3), (4096, 256, 2), (3000, 200, 1), (1001, 999, 2), (777, 333, 1)):
         Phi = rng.standard_normal((n, m))
         path = _dense_plan(plans, Phi, L, 1e-12, f"split_small_{n}_{m}_{L}")
         w = mi.Workload("sks", "mesh", n, m, "float64", 1e-12, L)
@@ -290,4 +290,41 @@ def test_split_k_small_blocks(gpu, oracle_lib, plans):
         assert torch.equal(a1, a2)
         ad = torch.from_numpy(Phi).cuda().T @ y[0]
         assert (torch.linalg.vector_norm(a1[0] - ad) / torch.linalg.vector_norm(ad)).item() < 1e-11
+        P.close()
+
+
+def test_persistent_matches_per_stage_launches(gpu, oracle_lib, plans):
+    """nrhs = 1 applies as one cooperative (persistent) launch per direction
+    and as one launch per stage give bitwise-identical results (same tiles,
+    same split order), for complex and real plans with aliases, COPY blocks,
+    split tiles and unfused sums; both match O2; repeated persistent applies
+    (work counters re-armed in-kernel) and graph replay stay identical."""
+    rng = np.random.default_rng(21)
+    cases = [flat_case(plans, 1024, 32, 4, 1e-15, name="exact"), flat_case(plans, 2048, 32, 4, 1e-8)]
+    Phi = rng.standard_normal((3000, 200))
+    cases.append((_dense_plan(plans, Phi, 1, 1e-12, "persist_tall"), mi.Workload("pt", "mesh", 3000, 200, "float64", 1e-12, 1)))
+    for path, w in cases:
+        P = gpu.Plan(path)
+        O = oracle_lib.Plan(path)
+        if w.dtype == "complex128":
+            c, y = mi.complex_gaussian(1, w.m, 401), mi.complex_gaussian(1, w.n, 402)
+        else:
+            c, y = mi.real_gaussian(1, w.m, 401), mi.real_gaussian(1, w.n, 402)
+        ct, yt = torch.from_numpy(c).cuda(), torch.from_numpy(y).cuda()
+        res = {}
+        for mode in (True, False):
+            P.set_persistent(mode)
+            for fused in (True, False):
+                P.set_fused_sums(fused)
+                f = [P.apply(ct).cpu() for _ in range(3)]
+                a = [P.adjoint(yt).cpu() for _ in range(3)]
+                assert all(torch.equal(f[0], x) for x in f[1:]) and all(torch.equal(a[0], x) for x in a[1:])
+                res[(mode, fused)] = (f[0], a[0])
+        for k in res:
+            assert torch.equal(res[k][0], res[(True, True)][0]), (path, k)
+            assert torch.equal(res[k][1], res[(True, True)][1]), (path, k)
+        assert rel_cols(res[(True, True)][0].numpy(), O.apply(c)) <= PARITY
+        assert rel_cols(res[(True, True)][1].numpy(), O.adjoint(y)) <= PARITY
+        P.set_persistent(True)
+        P.set_fused_sums(True)
         P.close()
