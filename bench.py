@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-table", action="store_true",
+                    help="cpu_baseline leg only: time the oracle (O2 at 1 and all threads, O1 dense sum full or on "
+                         "a labelled row subset) on this host for --workload, print one JSON line, exit")
     return ap.parse_args()
 
 
@@ -217,6 +220,55 @@ def run_reference(args, w, path):
     print(json.dumps(out), flush=True)
 
 
+def run_cpu_table(args, w, path):
+    """SURVEY.md §8(d) CPU protocol: O2 (butterfly) with all threads and with
+    one; O1 (dense sum) in full for c1 and c4, on a 4,096-row subset for the
+    others (extrapolated x n/4096, labelled).  Bounded: each figure is the
+    mean over reps within ~args.cpu_seconds."""
+    import oracle
+
+    out = {"impl": "cpu_table", "workload": workload_desc(w), "unit": "ms per column transform",
+           "host_cores": len(os.sched_getaffinity(0))}
+    try:
+        out["cpu_model"] = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:
+        pass
+    c = mi.workload_coefficients(w, 1)
+    y = mi.workload_adjoint_input(w, 1)
+    for threads in (oracle.num_threads(), 1):
+        oracle.set_threads(threads)
+        O = oracle.Plan(path, verify_checksum=False)
+        for kind, fn, arg in (("apply", O.apply, c), ("adjoint", O.adjoint, y)):
+            reps, t0 = 0, time.perf_counter()
+            while True:
+                fn(arg)
+                reps += 1
+                if time.perf_counter() - t0 >= args.cpu_seconds / 4 or reps >= 200:
+                    break
+            out[f"O2_{kind}_threads{threads}"] = 1e3 * (time.perf_counter() - t0) / reps
+        O.close()
+    oracle.set_threads(out["host_cores"])
+    rows = np.arange(w.n) if w.n * w.m <= 2**27 else np.sort(np.random.default_rng(7).choice(w.n, 4096, replace=False))
+    t0 = time.perf_counter()
+    if w.family == "flat":
+        oracle.flat_synth(mi.flat_points(w.n)[rows], mi.flat_modes(w.extra["side"])[: w.m], c)
+    elif w.family == "sphere":
+        th, ph, _ = mi.sphere_points(w.n)
+        oracle.sphere_synth(th[rows], ph[rows], w.extra["lmax"], c)
+    else:
+        from mht_inputs import mesh as mm
+
+        Phi = mm.torus_workload_inputs(w.extra["nu"], w.extra["nv"], w.m)[3]
+        t0 = time.perf_counter()
+        oracle.dense_synth(Phi[rows], c)
+    el = time.perf_counter() - t0
+    out["O1_synth_ms"] = 1e3 * el * w.n / len(rows)
+    out["O1_rows_timed"] = int(len(rows))
+    out["O1_note"] = ("full" if len(rows) == w.n else f"extrapolated from a {len(rows)}-row subset (x n/{len(rows)})")
+    out["threads_all"] = out["host_cores"]
+    print(json.dumps(out), flush=True)
+
+
 # ---------------------------------------------------------------- main
 def main():
     args = parse()
@@ -224,6 +276,10 @@ def main():
 
     w = mi.WORKLOADS[args.workload]
     ws, rank, lrank = dist_setup(args)
+    if args.cpu_table:
+        if rank == 0:
+            run_cpu_table(args, w, get_plan(w, args, 1, rank, lrank))
+        return
     if args.impl == "reference":
         # the reference arm (the oracle on host cores) runs on rank 0 only;
         # other ranks exit 0 without work

@@ -109,6 +109,40 @@ mht_status mht_apply_adjoint(mht_plan *plan, const void *f, void *c, int nrhs);
 mht_status mht_apply_host(mht_plan *plan, const void *c_host, void *f_host, int nrhs);
 mht_status mht_apply_adjoint_host(mht_plan *plan, const void *f_host, void *c_host, int nrhs);
 
+/* ---- applications on top of the transform (§7) ----------------
+ * A real diagonal on the coefficient side is fused into the transform's own
+ * loads of c (synthesis) or its final stores of c (analysis): no extra pass
+ * over c.  d / S: device float64 arrays of m entries in the plan's frequency
+ * order; the same diagonal for every right-hand side.
+ *
+ * Spectral filtering (§7.1):  f = Phi diag(F(lambda)) c. */
+mht_status mht_apply_diag(mht_plan *plan, const void *c, const double *d, void *f, int nrhs);
+/* Filtered analysis:  c = diag(d) Phi^* f. */
+mht_status mht_apply_adjoint_diag(mht_plan *plan, const void *f, const double *d, void *c, int nrhs);
+/* Gaussian random field samples (§7.2, Eq. KL-expansion):
+ * y = Phi sqrt(S) z with z ~ N(0, I) supplied by the caller (m x nrhs; for a
+ * complex plan, complex z); sqrt(S_k) is taken inside the fused load. */
+mht_status mht_grf_sample(mht_plan *plan, const void *z, const double *S, void *y, int nrhs);
+/* Covariance matrix-vector product (§7.2):  out = Phi S Phi^* v
+ * (v, out: n x nrhs).  Analysis with S fused into its final sums into a plan-
+ * owned m x nrhs buffer, then synthesis. */
+mht_status mht_covariance_apply(mht_plan *plan, const void *v, const double *S, void *out, int nrhs);
+
+/* Inverse MHT by LSQR (§7.1, Eq. inverse-MHT):
+ *   x = argmin_c ||Phi c - b||_2  for each of the nrhs columns of b.
+ * b: device n x nrhs; x: device m x nrhs (output; the iterate).  Paige &
+ * Saunders' LSQR from x_0 = 0; each iteration is one synthesis and one
+ * analysis of the plan plus fused vector kernels; all per-column scalars stay
+ * on the device.  Stops after max_iters, or earlier (checked every 10
+ * iterations) when every column satisfies Paige & Saunders' test 1
+ * ||r|| <= btol ||b|| + atol ||A|| ||x|| or test 2 ||A^* r|| <= atol ||A|| ||r||
+ * (atol = btol = 0: exactly max_iters iterations).  Optional host outputs:
+ * *iters_done, and per column rnorm[r] ~ ||b - Phi x||, arnorm[r] ~ ||Phi^*(b - Phi x)||
+ * (the recurrences' estimates).  Synchronises.  Allocates its work vectors
+ * (5 vectors of n or m x nrhs) per call. */
+mht_status mht_lsqr(mht_plan *plan, const void *b, void *x, int nrhs, int max_iters, double atol, double btol,
+                    int *iters_done, double *rnorm, double *arnorm);
+
 /* Capture each (direction, nrhs, c, f) apply sequence in a CUDA graph and
  * replay it on later calls with the same arguments (on = 1, default on). */
 mht_status mht_set_graphs(mht_plan *plan, int on);

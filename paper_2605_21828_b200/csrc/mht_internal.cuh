@@ -44,9 +44,10 @@ struct DevBlock {
   int64_t asp_off;  // split scratch base of this block's adjoint column tiles (scalars)
   int32_t ld;       // leading dimension of T in the device pool (r_out, rounded up to
                     // even for float64 so every column starts 16-byte aligned)
-  int32_t pad3;
+  int32_t mks;      // multi-RHS adjoint K (row) splits, 0 = none
+  int64_t msp_off;  // first split slab of this block's multi-RHS adjoint tiles
 };
-static_assert(sizeof(DevBlock) == 136, "DevBlock layout");
+static_assert(sizeof(DevBlock) == 144, "DevBlock layout");
 
 // Device repack of one block's factor (real plans): column-major r_out x ncols
 // with ld = r_out  ->  ld = dst_ld (>= r_out), padding rows zero.
@@ -84,7 +85,12 @@ struct Ctx {  // per-launch pointers
   const void *fin; // f input (adjoint)
   void *fout;      // f output (forward)
   void *fsplit;    // forward split-K partial rows
+  void *msplit;    // multi-RHS adjoint split slabs: [slab][64 columns][nrhs]
+  int *mcount;     // multi-RHS adjoint split arrival counters [group][rhs chunk]
   int *fcount;     // forward split-K arrival counters (zero between applies)
+  const double *diag;    // optional real diagonal on the coefficient side (m entries):
+                         // forward reads c_k * g(d_k), adjoint writes g(d_k) * c_k
+  int diag_sqrt;         // g(d) = sqrt(d) (GRF sampling) instead of d
   const int64_t *rdtab;  // fused adjoint sums: reader partial offsets
   int fused;             // 1: adjoint inputs are summed from the partials on load
   int64_t m, n, Zt, Pt;  // Zt/Pt: workspace entries per RHS (layout [entry][rhs])
@@ -114,6 +120,25 @@ struct Phase {
 };
 constexpr int PERSIST_THREADS = 128;
 
+
+// LSQR per-column state (device resident; mht_lsqr.cu)
+struct LsqrCol {
+  double alpha, beta, rhobar, phibar, cs;
+  double step_x, step_w;        // x += step_x w;  w = v - step_w w
+  double rnorm, arnorm, anorm2, bnorm, xnorm;
+};
+
+// LSQR vector kernels (mht_lsqr.cu).  stage: 0 beta / 1 alpha + rotation /
+// 2 initial beta / 3 initial alpha.  which: 0 alpha, 1 beta (axpy); 0 beta,
+// 1 alpha (scale).
+int lsqr_partials(int64_t len);
+void lsqr_axpy_norm(bool cplx, const void *y, void *u, int64_t len, int k, const LsqrCol *col, int which,
+                    double *partial, void *stream);
+void lsqr_scalars(const double *partial, int nblk, int k, LsqrCol *col, int stage, void *stream);
+void lsqr_scale(bool cplx, void *u, int64_t len, int k, const LsqrCol *col, int which, void *stream);
+void lsqr_update(bool cplx, void *v, void *w, void *x, int64_t len, int k, const LsqrCol *col, int first,
+                 void *stream);
+void lsqr_xnorm(bool cplx, const void *x, int64_t len, int k, double *partial, LsqrCol *col, void *stream);
 
 // Launchers (mht_kernels.cu).  is_complex selects double2 vs double.
 void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, void *stream);

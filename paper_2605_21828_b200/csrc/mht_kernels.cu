@@ -36,6 +36,7 @@ struct Tr<double> {
   static __device__ __forceinline__ void fma(double &a, double t, double x) { a = ::fma(t, x, a); }
   static __device__ __forceinline__ void fmac(double &a, double t, double z) { a = ::fma(t, z, a); }
   static __device__ __forceinline__ double add(double a, double b) { return a + b; }
+  static __device__ __forceinline__ double scale(double a, double d) { return a * d; }
   static __device__ __forceinline__ double shfl(double v, int s) { return __shfl_sync(FULL, v, s); }
   static __device__ __forceinline__ double shfl_xor(double v, int s) {
     return __shfl_xor_sync(FULL, v, s);
@@ -74,6 +75,7 @@ struct Tr<double2> {
   static __device__ __forceinline__ double2 add(double2 a, double2 b) {
     return make_double2(a.x + b.x, a.y + b.y);
   }
+  static __device__ __forceinline__ double2 scale(double2 a, double d) { return make_double2(a.x * d, a.y * d); }
   static __device__ __forceinline__ double2 shfl(double2 v, int s) {
     return make_double2(__shfl_sync(FULL, v.x, s), __shfl_sync(FULL, v.y, s));
   }
@@ -89,6 +91,14 @@ struct Tr<double2> {
 };
 
 // in[q] for right-hand side r: two segments, each in c (ld m) or zpool (ld Zt).
+// Coefficient-side diagonal (spectral filter F(lambda_k), GRF sqrt S(lambda_k),
+// covariance S; §7.1, §7.2), fused into the
+// loads of c (forward) and the stores of c (adjoint).
+__device__ __forceinline__ double diag_at(const Ctx &cx, int64_t k) {
+  const double d = cx.diag[k];
+  return cx.diag_sqrt ? sqrt(d) : d;
+}
+
 // CG: read the workspace through L2 only (ld.global.cg).  The persistent
 // kernel writes and reads workspace in different phases of ONE launch, and L1
 // is not coherent: a line cached while reading one stage's z could be stale
@@ -98,7 +108,10 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
   const bool s1 = q >= B.seg_len[0];  // no dynamic indexing: keeps B in registers
   const int64_t off = s1 ? B.seg_off[1] + (q - B.seg_len[0]) : B.seg_off[0] + q;
   const int32_t src = s1 ? B.seg_src[1] : B.seg_src[0];
-  if (src == SRC_C) return static_cast<const S *>(cx.c)[r * cx.m + off];  // user layout: column-major
+  if (src == SRC_C) {  // user layout: column-major
+    const S v = static_cast<const S *>(cx.c)[r * cx.m + off];
+    return cx.diag ? Tr<S>::scale(v, diag_at(cx, off)) : v;
+  }
   const S *p = static_cast<const S *>(cx.z) + off * cx.nrhs + r;           // workspace: RHS-fastest
   if constexpr (CG) return Tr<S>::ldcg(p);
   return *p;
@@ -112,7 +125,8 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
 // row sums to scratch and the last CTA of the group to arrive (atomic counter)
 // adds them in split order — deterministic, no float atomics.
 // ------------------------------------------------------------------------
-template <class S>
+// CG: workspace reads through L2 only (the persistent kernel; see in_value)
+template <class S, bool CG>
 __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
   using X = Tr<S>;
   const DevBlock B = cx.blocks[tl.blk];
@@ -140,7 +154,7 @@ __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
     S xr = X::zero();
     if (j < jend) {
       const int q = (B.flags & F_RED_IOTA) ? j : cx.idx[B.red_off + j];
-      xr = in_value<S, true>(cx, B, q, 0);
+      xr = in_value<S, CG>(cx, B, q, 0);
     }
     const int jn = min(32, jend - j0);
     const S *col = T + (int64_t)j0 * ld;
@@ -209,7 +223,7 @@ __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
     const int row = tl.start + i;
     if (row < B.n_skel) {
       const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
-      s = X::add(s, in_value<S, true>(cx, B, q, 0));
+      s = X::add(s, in_value<S, CG>(cx, B, q, 0));
     }
     if (B.flags & F_OUT_F)
       static_cast<S *>(cx.fout)[cx.perm[B.out_off + row]] = s;
@@ -221,7 +235,7 @@ __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
 
 template <class S>
 __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Tile *__restrict__ tiles) {
-  fwd_tile<S>(cx, tiles[blockIdx.y]);
+  fwd_tile<S, false>(cx, tiles[blockIdx.y]);
 }
 
 // adjoint input z[i] of a block: f through perm_x (leaf stage), else the group
@@ -257,7 +271,7 @@ __device__ __forceinline__ S adj_in(const Ctx &cx, const DevBlock &B, int i, int
 // partial column sums to scratch and the last CTA of the group to arrive adds
 // them in split order (deterministic, no float atomics).
 // ------------------------------------------------------------------------
-template <class S, int RB>
+template <class S, int RB, bool CG>
 __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_f, int rhs0) {
   using X = Tr<S>;
   // columns per warp: 8 complex / 16 real
@@ -290,7 +304,7 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
     const int rn = min(ADJ_RCH, rend - rc);
     for (int e = threadIdx.x; e < rn * RB; e += ADJ_THREADS) {
       const int i = e % rn, k = e / rn;
-      zs[i][k] = (rhs0 + k < cx.nrhs) ? adj_in<S, true>(cx, B, rc + i, rhs0 + k, from_f) : X::zero();
+      zs[i][k] = (rhs0 + k < cx.nrhs) ? adj_in<S, CG>(cx, B, rc + i, rhs0 + k, from_f) : X::zero();
     }
     if (REAL && (rn & 1) && threadIdx.x < RB) zs[rn][threadIdx.x] = X::zero();  // pair partner of the last row
     __syncthreads();
@@ -335,7 +349,7 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
       const int i = e % B.n_skel, k = e / B.n_skel;
       if (rhs0 + k >= cx.nrhs) continue;
       const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
-      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0 + k] = adj_in<S, true>(cx, B, i, rhs0 + k, from_f);
+      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0 + k] = adj_in<S, CG>(cx, B, i, rhs0 + k, from_f);
     }
   }
   // warp reductions
@@ -388,7 +402,7 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
 template <class S, int RB>
 __global__ void __launch_bounds__(ADJ_THREADS, 7) adj_kernel(const Ctx cx, const Tile *__restrict__ tiles,
                                                              int from_f) {
-  adj_tile<S, RB>(cx, tiles[blockIdx.y], from_f, blockIdx.x * RB);
+  adj_tile<S, RB, false>(cx, tiles[blockIdx.y], from_f, blockIdx.x * RB);
 }
 
 // ------------------------------------------------------------------------
@@ -474,7 +488,16 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
   const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
   const int64_t ld = B.ld;
   const int K = ADJ ? B.r_out : B.n_red;
-  const int nchunks = (K + BK - 1) / BK;
+  // adjoint K split (tall blocks on low-parallelism stages): rows [kbeg, kend)
+  const bool ksplit = ADJ && tl.pad >= 0;
+  const int sidx = ksplit ? (tl.pad & 255) : 0;
+  int kbeg = 0, kend = K;
+  if (ksplit) {
+    const int chunk = ((K + B.mks - 1) / B.mks + BK - 1) / BK * BK;
+    kbeg = min(K, sidx * chunk);
+    kend = min(K, kbeg + chunk);
+  }
+  const int nchunks = (kend - kbeg + BK - 1) / BK;
   const bool red_iota = (B.flags & F_RED_IOTA) != 0;
 
   // Operand staging.  Thread e writes fragment slot e (contiguous, conflict-free
@@ -482,14 +505,14 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
   // m = 16 w + 8 hi + gid and k = 4 k4 + tig, so a warp reads 4 (forward) or 8
   // (adjoint) fully used 128/64-byte global segments.
   auto load_A = [&](int kc) {
-    const int kb = kc * BK;
+    const int kb = kbeg + kc * BK;
     S *dst = As + (kc % NB) * A_CH;
 #pragma unroll
     for (int i = 0; i < MM_BM * BK / MM_THREADS; ++i) {
       const int e = threadIdx.x + MM_THREADS * i;
       const int tig_ = e & 3, gid_ = (e >> 2) & 7, hi = (e >> 5) & 1, w = (e >> 6) & (AW - 1), k4 = e >> 8;
       const int m = w * 16 + hi * 8 + gid_, k = k4 * 4 + tig_;
-      const bool ok = m < tl.count && kb + k < K;
+      const bool ok = m < tl.count && kb + k < kend;
       const S *src = ADJ ? T + (int64_t)(tl.start + m) * ld + (kb + k) : T + (int64_t)(kb + k) * ld + (tl.start + m);
       cp_async<sizeof(S)>(dst + e, ok ? src : T, ok);
     }
@@ -499,17 +522,17 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
   int qreg[B_PER_T];
   auto load_q = [&](int kc) {
     if (ADJ) return;
-    const int kb = kc * BK;
+    const int kb = kbeg + kc * BK;
 #pragma unroll
     for (int i = 0; i < B_PER_T; ++i) {
       const int e = threadIdx.x + MM_THREADS * i;
       const int k = ((e >> 5) / NT) * 4 + (e & 3);
-      qreg[i] = (kb + k < K) ? (red_iota ? kb + k : __ldg(cx.idx + B.red_off + kb + k)) : 0;
+      qreg[i] = (kb + k < kend) ? (red_iota ? kb + k : __ldg(cx.idx + B.red_off + kb + k)) : 0;
     }
   };
   S breg[B_PER_T];
   auto load_B = [&](int kc) {
-    const int kb = kc * BK;
+    const int kb = kbeg + kc * BK;
 #pragma unroll
     for (int i = 0; i < B_PER_T; ++i) {
       const int e = threadIdx.x + MM_THREADS * i;
@@ -517,7 +540,7 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
       const int k = k4 * 4 + tig_, n = t * 8 + gid_;
       const int r = rhs0 + n;
       S v = X::zero();
-      if (kb + k < K && r < cx.nrhs) v = ADJ ? adj_in<S>(cx, B, kb + k, r, from_f != 0) : in_value<S>(cx, B, qreg[i], r);
+      if (kb + k < kend && r < cx.nrhs) v = ADJ ? adj_in<S>(cx, B, kb + k, r, from_f != 0) : in_value<S>(cx, B, qreg[i], r);
       breg[i] = v;
     }
   };
@@ -614,19 +637,47 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
           static_cast<S *>(cx.fout)[r * cx.n + cx.perm[B.out_off + row]] = val;
         else
           static_cast<S *>(cx.z)[(B.out_off + row) * cx.nrhs + r] = val;
+      } else if (ksplit) {
+        const int64_t slab = B.msp_off + (int64_t)(tl.start / MMA_COLS) * B.mks + sidx;
+        static_cast<S *>(cx.msplit)[(slab * MMA_COLS + m) * cx.nrhs + r] = val;
       } else {
         const int q = red_iota ? row : cx.idx[B.red_off + row];
         static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = val;
       }
     }
   }
-  if (ADJ && tl.start == 0 && B.n_skel > 0) {
+  if (ADJ && tl.start == 0 && sidx == 0 && B.n_skel > 0) {
     for (int e = threadIdx.x; e < B.n_skel * NRT; e += MM_THREADS) {
       const int i = e % B.n_skel, r = rhs0 + e / B.n_skel;
       if (r >= cx.nrhs) continue;
       const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
       static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = adj_in<S>(cx, B, i, r, from_f != 0);
     }
+  }
+  if (ADJ && ksplit) {
+    // the last split of (block, column tile, RHS chunk) to arrive sums the
+    // slabs in split order (deterministic) and writes the partials
+    int &last = *reinterpret_cast<int *>(As);  // operand buffers are free after the K loop
+    __threadfence();
+    __syncthreads();
+    const int grp = tl.pad >> 8;
+    int *cnt = cx.mcount + (int64_t)grp * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0) last = atomicAdd(cnt, 1) == B.mks - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int64_t slab0 = B.msp_off + (int64_t)(tl.start / MMA_COLS) * B.mks;
+    const S *scr = static_cast<const S *>(cx.msplit);
+    for (int e = threadIdx.x; e < tl.count * NRT; e += MM_THREADS) {
+      const int m = e / NRT, r = rhs0 + e % NRT;
+      if (r >= cx.nrhs) continue;
+      S sum = X::zero();
+      for (int k = 0; k < B.mks; ++k) sum = X::add(sum, X::ldcg(scr + ((slab0 + k) * MMA_COLS + m) * cx.nrhs + r));
+      const int row = tl.start + m;
+      const int q = red_iota ? row : cx.idx[B.red_off + row];
+      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = sum;
+    }
+    if (threadIdx.x == 0) *cnt = 0;  // re-arm for the next apply
   }
 }
 
@@ -688,7 +739,7 @@ __device__ __forceinline__ void reduce_piece(const Ctx &cx, const Piece p, const
       s = X::add(s, CG ? X::ldcg(a) : *a);
     }
     if (p.dst_src == SRC_C)
-      static_cast<S *>(cx.cw)[r * cx.m + p.dst_off + i] = s;
+      static_cast<S *>(cx.cw)[r * cx.m + p.dst_off + i] = cx.diag ? X::scale(s, diag_at(cx, p.dst_off + i)) : s;
     else
       static_cast<S *>(cx.z)[(p.dst_off + i) * nr + r] = s;
   }
@@ -732,9 +783,9 @@ __global__ void __launch_bounds__(PERSIST_THREADS, MINB) persist_kernel(const Ct
       __syncthreads();
       if (t >= ph.count) break;
       if (ph.kind == PH_FWD)
-        fwd_tile<S>(cx, ftiles[ph.off + t]);
+        fwd_tile<S, true>(cx, ftiles[ph.off + t]);
       else if (ph.kind == PH_ADJ)
-        adj_tile<S, 1>(cx, atiles[ph.off + t], ph.from_f, 0);
+        adj_tile<S, 1, true>(cx, atiles[ph.off + t], ph.from_f, 0);
       else
         reduce_piece<S, true>(cx, pieces[ph.off + t], rd);
       __syncthreads();

@@ -75,13 +75,22 @@ struct mht_plan {
     int dir, nrhs;
     const void *src;
     void *dst;
+    const double *diag;
+    int diag_sqrt;
     bool operator<(const GraphKey &o) const {
       if (dir != o.dir) return dir < o.dir;
       if (nrhs != o.nrhs) return nrhs < o.nrhs;
       if (src != o.src) return src < o.src;
-      return dst < o.dst;
+      if (dst != o.dst) return dst < o.dst;
+      if (diag != o.diag) return diag < o.diag;
+      return diag_sqrt < o.diag_sqrt;
     }
   };
+  // coefficient-side diagonal of the current call (mht_apply_diag & co.)
+  const double *cur_diag = nullptr;
+  int cur_diag_sqrt = 0;
+  void *d_ctmp = nullptr;  // m x nrhs scratch for mht_covariance_apply
+  int ctmp_nrhs = 0;
   std::map<GraphKey, cudaGraphExec_t> gcache;
   cudaStream_t cap_stream = nullptr;
   void clear_graphs() {
@@ -121,6 +130,10 @@ struct mht_plan {
   bool fused_sum = true;        // adjoint group sums on the consumer's load (MHT_FUSED_SUM=0: off)
   int n_unfused = 0;
   int64_t n_split_groups = 0;
+  int64_t m_slabs = 0;    // multi-RHS adjoint split slabs (64 columns x nrhs each)
+  int32_t m_groups = 0;   // multi-RHS adjoint split groups
+  void *d_msplit = nullptr;
+  int *d_mcount = nullptr;
   Range cpieces;
   std::vector<int64_t> stage_coef_bytes;
   std::vector<int32_t> stage_nmat;
@@ -147,7 +160,7 @@ struct mht_plan {
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd, (void *)d_fwd1, d_fsplit, (void *)d_fcount,
-                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, (void *)d_phases, (void *)d_ctr, (void *)d_stamps, d_z, d_part, d_hc, d_hf})
+                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, (void *)d_phases, (void *)d_ctr, (void *)d_stamps, d_msplit, (void *)d_mcount, d_ctmp, d_z, d_part, d_hc, d_hf})
       if (p) cudaFree(p);
   }
 };
@@ -539,6 +552,11 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
   if (const char *e = getenv("MHT_ASPLIT_MIN")) ADJ1_MIN_SPLIT = std::max(32, atoi(e));
   int64_t asplit_scalars = 0;
   int32_t agroups = 0;
+  const int MMA_TARGET = prop.multiProcessorCount * 4;
+  int MMA_MIN_SPLIT = 256;
+  if (const char *e = getenv("MHT_MSPLIT_MIN")) MMA_MIN_SPLIT = std::max(64, atoi(e));
+  int64_t mslabs = 0;
+  int32_t mgroups = 0;
   P->fwd.assign(L + 2, Range{});
   P->adj.assign(L + 2, Range{});
   P->adjm.assign(L + 2, Range{});
@@ -591,9 +609,41 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
       P->adj[s] = Range{(int32_t)adj_all.size(), (int32_t)lst.size()};
       for (auto &x : lst) adj_all.push_back(x.second);
     }
-    std::stable_sort(amt[s].begin(), amt[s].end(), by_cost);
-    P->adjm[s] = Range{(int32_t)adjm_all.size(), (int32_t)amt[s].size()};
-    for (auto &x : amt[s]) adjm_all.push_back(x.second);
+    // multi-RHS adjoint K splits: on a stage with too few 64-column tiles to
+    // fill the GPU several times over, a tile of a tall block would run one
+    // long K loop; its rows are split into chunks of >= MMA_MIN_SPLIT (slabs
+    // summed in order by the last CTA of the group).
+    {
+      const int nt = (int)amt[s].size();
+      std::vector<std::pair<int64_t, Tile>> lst;
+      for (auto &x : amt[s]) {
+        DevBlock &D = blocks[x.second.blk];
+        int ks = 1;
+        if (nt > 0 && nt < MMA_TARGET && x.second.count > 0 && D.r_out >= 2 * MMA_MIN_SPLIT)
+          ks = std::min(16, D.r_out / MMA_MIN_SPLIT);
+        if (ks <= 1) {
+          lst.push_back(x);
+          continue;
+        }
+        if (D.mks == 0) {
+          D.mks = ks;
+          D.msp_off = mslabs;
+          mslabs += (int64_t)((D.n_red + MMA_COLS - 1) / MMA_COLS) * ks;
+        }
+        const int bk = P->cplx ? 16 : 32;
+        const int chunk = ((D.r_out + ks - 1) / ks + bk - 1) / bk * bk;
+        for (int k = 0; k < ks; ++k) {
+          const int rows = std::max(0, std::min(D.r_out, (k + 1) * chunk) - k * chunk);
+          Tile t = x.second;
+          t.pad = (mgroups << 8) | k;
+          lst.push_back({(int64_t)t.count * (rows + 4) + (k == 0 && t.start == 0 ? D.n_skel : 0), t});
+        }
+        ++mgroups;
+      }
+      std::stable_sort(lst.begin(), lst.end(), by_cost);
+      P->adjm[s] = Range{(int32_t)adjm_all.size(), (int32_t)lst.size()};
+      for (auto &x : lst) adjm_all.push_back(x.second);
+    }
   }
 
   // ------------------------------------------------ nrhs = 1 forward split-K
@@ -646,6 +696,8 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
     for (auto &x : lst) fwd1_all.push_back(x.second);
   }
   P->n_split_groups = groups;
+  P->m_slabs = mslabs;
+  P->m_groups = mgroups;
 
   // ------------------------------------------------ adjoint group-sum pieces
   // Readers: every materialised block's input segments.  For a source range
@@ -873,6 +925,14 @@ mht_status ensure_ws(mht_plan *P, int nrhs) {
   P->ws_nrhs = 0;
   CUDA_TRY(cudaMalloc(&P->d_z, (size_t)P->Zt * nrhs * P->ssz));
   CUDA_TRY(cudaMalloc(&P->d_part, (size_t)P->Pt * nrhs * P->ssz));
+  if (P->d_msplit) cudaFree(P->d_msplit);
+  if (P->d_mcount) cudaFree(P->d_mcount);
+  P->d_msplit = nullptr;
+  P->d_mcount = nullptr;
+  CUDA_TRY(cudaMalloc(&P->d_msplit, (size_t)std::max<int64_t>(1, P->m_slabs * MMA_COLS * nrhs) * P->ssz));
+  const size_t ncnt = (size_t)std::max<int64_t>(1, (int64_t)P->m_groups * ((nrhs + 7) / 8));
+  CUDA_TRY(cudaMalloc((void **)&P->d_mcount, ncnt * sizeof(int)));
+  CUDA_TRY(cudaMemset(P->d_mcount, 0, ncnt * sizeof(int)));
   P->ws_nrhs = nrhs;
   return MHT_OK;
 }
@@ -889,6 +949,10 @@ Ctx make_ctx(mht_plan *P, int nrhs) {
   cx.fsplit = P->d_fsplit;
   cx.fcount = P->d_fcount;
   cx.rdtab = P->d_rdtab;
+  cx.diag = P->cur_diag;
+  cx.diag_sqrt = P->cur_diag_sqrt;
+  cx.msplit = P->d_msplit;
+  cx.mcount = P->d_mcount;
   // fused group sums only at nrhs = 1: the multi-RHS gathers measured faster
   // from the reduced workspace (profiles/r01_fused_sums_ab.txt)
   cx.fused = (P->fused_sum && nrhs == 1) ? 1 : 0;
@@ -1007,7 +1071,7 @@ mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
 // CUDA graph.  Profiling bypasses graphs (per-launch events).
 mht_status run_dir(mht_plan *P, int dir, const void *src, void *dst, int nrhs) {
   if (!P->graphs || P->prof) return dir == 0 ? run_forward(P, src, dst, nrhs) : run_adjoint(P, src, dst, nrhs);
-  mht_plan::GraphKey key{dir, nrhs, src, dst};
+  mht_plan::GraphKey key{dir, nrhs, src, dst, P->cur_diag, P->cur_diag_sqrt};
   auto it = P->gcache.find(key);
   if (it == P->gcache.end()) {
     if (!P->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&P->cap_stream, cudaStreamNonBlocking));
@@ -1110,6 +1174,155 @@ mht_status mht_apply_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
   mht_status s = ensure_ws(P, nrhs);
   if (s != MHT_OK) return s;
   return run_dir(P, 1, f, c, nrhs);
+}
+
+namespace {
+struct DiagScope {  // sets the plan's coefficient-side diagonal for one call
+  mht_plan *P;
+  DiagScope(mht_plan *p, const double *d, int sq) : P(p) {
+    P->cur_diag = d;
+    P->cur_diag_sqrt = sq;
+  }
+  ~DiagScope() {
+    P->cur_diag = nullptr;
+    P->cur_diag_sqrt = 0;
+  }
+};
+}  // namespace
+
+mht_status mht_apply_diag(mht_plan *P, const void *c, const double *d, void *f, int nrhs) {
+  if (!P || !c || !d || !f || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s = ensure_ws(P, nrhs);
+  if (s != MHT_OK) return s;
+  DiagScope ds(P, d, 0);
+  return run_dir(P, 0, c, f, nrhs);
+}
+
+mht_status mht_apply_adjoint_diag(mht_plan *P, const void *f, const double *d, void *c, int nrhs) {
+  if (!P || !c || !d || !f || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s = ensure_ws(P, nrhs);
+  if (s != MHT_OK) return s;
+  DiagScope ds(P, d, 0);
+  return run_dir(P, 1, f, c, nrhs);
+}
+
+mht_status mht_grf_sample(mht_plan *P, const void *z, const double *S, void *y, int nrhs) {
+  if (!P || !z || !S || !y || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s = ensure_ws(P, nrhs);
+  if (s != MHT_OK) return s;
+  DiagScope ds(P, S, 1);
+  return run_dir(P, 0, z, y, nrhs);
+}
+
+mht_status mht_covariance_apply(mht_plan *P, const void *v, const double *S, void *out, int nrhs) {
+  if (!P || !v || !S || !out || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s = ensure_ws(P, nrhs);
+  if (s != MHT_OK) return s;
+  if (nrhs > P->ctmp_nrhs) {
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    P->clear_graphs();
+    if (P->d_ctmp) cudaFree(P->d_ctmp);
+    P->d_ctmp = nullptr;
+    P->ctmp_nrhs = 0;
+    CUDA_TRY(cudaMalloc(&P->d_ctmp, (size_t)P->m * nrhs * P->ssz));
+    P->ctmp_nrhs = nrhs;
+  }
+  {
+    DiagScope ds(P, S, 0);  // c = S Phi^* v  (diagonal fused into the adjoint's final sums)
+    if ((s = run_dir(P, 1, v, P->d_ctmp, nrhs)) != MHT_OK) return s;
+  }
+  return run_dir(P, 0, P->d_ctmp, out, nrhs);  // out = Phi c
+}
+
+// ---------------------------------------------------------------- LSQR
+// Inverse MHT (§7.1, Eq. inverse-MHT): Paige &
+// Saunders' LSQR on Phi, every iteration = one synthesis + one analysis of
+// the plan plus the vector kernels of mht_lsqr.cu; per-column scalars stay on
+// the device.  Convergence is checked every `check_every` iterations
+// (one small device-to-host copy).
+mht_status mht_lsqr(mht_plan *P, const void *b, void *x, int nrhs, int max_iters, double atol, double btol,
+                    int *iters_done, double *rnorm, double *arnorm) {
+  if (!P || !b || !x || nrhs < 1 || max_iters < 0) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status st = ensure_ws(P, nrhs);
+  if (st != MHT_OK) return st;
+  const int64_t n = P->n, m = P->m;
+  const size_t sz = P->ssz;
+  const int pn = lsqr_partials(n), pm = lsqr_partials(m);
+  const int pmax = std::max(pn, pm);
+  struct Buf {
+    void *p = nullptr;
+    ~Buf() {
+      if (p) cudaFree(p);
+    }
+  } u, v, w, tn, tm, part, col;
+  CUDA_TRY(cudaMalloc(&u.p, (size_t)n * nrhs * sz));
+  CUDA_TRY(cudaMalloc(&v.p, (size_t)m * nrhs * sz));
+  CUDA_TRY(cudaMalloc(&w.p, (size_t)m * nrhs * sz));
+  CUDA_TRY(cudaMalloc(&tn.p, (size_t)n * nrhs * sz));
+  CUDA_TRY(cudaMalloc(&tm.p, (size_t)m * nrhs * sz));
+  CUDA_TRY(cudaMalloc(&part.p, (size_t)pmax * nrhs * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&col.p, (size_t)nrhs * sizeof(LsqrCol)));
+  CUDA_TRY(cudaMemsetAsync(col.p, 0, (size_t)nrhs * sizeof(LsqrCol), P->stream));
+  LsqrCol *dc = static_cast<LsqrCol *>(col.p);
+  double *dp = static_cast<double *>(part.p);
+  void *s = P->stream;
+  const bool cx = P->cplx;
+  // beta_1 u_1 = b;  alpha_1 v_1 = Phi^* u_1;  w_1 = v_1;  x_0 = 0
+  lsqr_axpy_norm(cx, b, u.p, n, nrhs, nullptr, 0, dp, s);
+  lsqr_scalars(dp, pn, nrhs, dc, 2, s);
+  lsqr_scale(cx, u.p, n, nrhs, dc, 0, s);
+  if ((st = run_dir(P, 1, u.p, v.p, nrhs)) != MHT_OK) return st;
+  lsqr_axpy_norm(cx, v.p, v.p, m, nrhs, nullptr, 0, dp, s);
+  lsqr_scalars(dp, pm, nrhs, dc, 3, s);
+  lsqr_update(cx, v.p, w.p, x, m, nrhs, dc, 1, s);
+  CUDA_TRY(cudaGetLastError());
+  const bool check = atol > 0 || btol > 0;
+  const int every = 10;
+  std::vector<LsqrCol> h(nrhs);
+  int it = 0;
+  for (; it < max_iters; ++it) {
+    // beta u = Phi v - alpha u
+    if ((st = run_dir(P, 0, v.p, tn.p, nrhs)) != MHT_OK) return st;
+    lsqr_axpy_norm(cx, tn.p, u.p, n, nrhs, dc, 0, dp, s);
+    lsqr_scalars(dp, pn, nrhs, dc, 0, s);
+    lsqr_scale(cx, u.p, n, nrhs, dc, 0, s);
+    // alpha v = Phi^* u - beta v, rotation, x / w updates
+    if ((st = run_dir(P, 1, u.p, tm.p, nrhs)) != MHT_OK) return st;
+    lsqr_axpy_norm(cx, tm.p, v.p, m, nrhs, dc, 1, dp, s);
+    lsqr_scalars(dp, pm, nrhs, dc, 1, s);
+    lsqr_update(cx, v.p, w.p, x, m, nrhs, dc, 0, s);
+    if (check && ((it + 1) % every == 0 || it + 1 == max_iters)) {
+      lsqr_xnorm(cx, x, m, nrhs, dp, dc, s);
+      CUDA_TRY(cudaMemcpyAsync(h.data(), dc, (size_t)nrhs * sizeof(LsqrCol), cudaMemcpyDeviceToHost,
+                               (cudaStream_t)s));
+      CUDA_TRY(cudaStreamSynchronize((cudaStream_t)s));
+      bool all = true;
+      for (const LsqrCol &c : h) {
+        const double an = sqrt(c.anorm2);
+        const bool t1 = c.rnorm <= btol * c.bnorm + atol * an * c.xnorm;
+        const bool t2 = c.arnorm <= atol * an * c.rnorm;
+        all = all && (t1 || t2);
+      }
+      if (all) {
+        ++it;
+        break;
+      }
+    }
+  }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(h.data(), dc, (size_t)nrhs * sizeof(LsqrCol), cudaMemcpyDeviceToHost, (cudaStream_t)s));
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)s));
+  if (iters_done) *iters_done = it;
+  for (int r = 0; r < nrhs; ++r) {
+    if (rnorm) rnorm[r] = h[r].rnorm;
+    if (arnorm) arnorm[r] = h[r].arnorm;
+  }
+  return MHT_OK;
 }
 
 static mht_status ensure_host_staging(mht_plan *P, int nrhs) {

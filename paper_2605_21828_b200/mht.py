@@ -22,7 +22,8 @@ LIB_PATH = os.path.join(HERE, "libmht.so")
 MHT_DTYPE_F64, MHT_DTYPE_C128 = 1, 2
 EXPORTED = [
     "mht_plan_load", "mht_plan_info_get", "mht_plan_set_stream", "mht_reserve", "mht_apply",
-    "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host", "mht_set_graphs", "mht_set_fused_sums", "mht_set_persistent", "mht_phase_times", "mht_sync",
+    "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host", "mht_apply_diag", "mht_apply_adjoint_diag", "mht_grf_sample", "mht_covariance_apply", "mht_lsqr",
+    "mht_set_graphs", "mht_set_fused_sums", "mht_set_persistent", "mht_phase_times", "mht_sync",
     "mht_stage_stats", "mht_set_profiling", "mht_profile_get", "mht_profile_reset", "mht_plan_destroy",
     "mht_status_string", "mht_last_error", "mht_build_info",
 ]
@@ -58,6 +59,10 @@ def load_library(path: str = LIB_PATH):
     L.mht_reserve.argtypes = [vp, i32]
     for nm in ("mht_apply", "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host"):
         getattr(L, nm).argtypes = [vp, vp, vp, i32]
+    for nm in ("mht_apply_diag", "mht_apply_adjoint_diag", "mht_grf_sample", "mht_covariance_apply"):
+        getattr(L, nm).argtypes = [vp, vp, vp, vp, i32]
+    L.mht_lsqr.argtypes = [vp, vp, vp, i32, i32, C.c_double, C.c_double, C.POINTER(C.c_int32),
+                           C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.mht_set_graphs.argtypes = [vp, i32]
     L.mht_set_fused_sums.argtypes = [vp, i32]
     L.mht_set_persistent.argtypes = [vp, i32]
@@ -175,6 +180,60 @@ class Plan:
         self._stream()
         mht_apply_adjoint(self._h, f2, c, nrhs, self.n, self.m, self.torch_dtype)
         return c
+
+    # ---- applications (§7): a real coefficient-side diagonal fused
+    # into the transform's own loads / stores of c (include/mht.h)
+    def _diag_ptr(self, d):
+        import torch
+
+        if not isinstance(d, torch.Tensor) or not d.is_cuda or d.dtype != torch.float64 or not d.is_contiguous() \
+                or d.numel() != self.m:
+            raise MhtError(f"expected a contiguous CUDA float64 tensor of {self.m} entries")
+        return C.c_void_p(d.data_ptr())
+
+    def _call4(self, name, x, rows_in, d, rows_out, out):
+        import torch
+
+        x2 = x.reshape(-1, rows_in) if x.dim() != 2 else x
+        nrhs = x2.shape[0]
+        y = out if out is not None else torch.empty((nrhs, rows_out), dtype=self.torch_dtype, device=self.device)
+        self._stream()
+        _check(getattr(load_library(), name)(self._h, _dev_ptr(x2, rows_in, nrhs, self.torch_dtype), self._diag_ptr(d),
+                                             _dev_ptr(y, rows_out, nrhs, self.torch_dtype), nrhs), name)
+        return y
+
+    def apply_diag(self, c, d, out=None):
+        """f = Phi diag(d) c  (spectral filter F(lambda_k) = d_k, §7.1)."""
+        return self._call4("mht_apply_diag", c, self.m, d, self.n, out)
+
+    def adjoint_diag(self, f, d, out=None):
+        """c = diag(d) Phi^* f."""
+        return self._call4("mht_apply_adjoint_diag", f, self.n, d, self.m, out)
+
+    def grf_sample(self, z, S, out=None):
+        """y = Phi sqrt(S) z  (Karhunen-Loeve sample, §7.2; z supplied by the caller)."""
+        return self._call4("mht_grf_sample", z, self.m, S, self.n, out)
+
+    def covariance_apply(self, v, S, out=None):
+        """out = Phi S Phi^* v  (covariance matvec, §7.2)."""
+        return self._call4("mht_covariance_apply", v, self.n, S, self.n, out)
+
+    def lsqr(self, b, max_iters: int, atol: float = 0.0, btol: float = 0.0, out=None):
+        """Inverse MHT x = argmin ||Phi x - b|| by LSQR (§7.1).  Returns
+        (x, iterations, rnorm[nrhs], arnorm[nrhs])."""
+        import torch
+
+        b2 = b.reshape(-1, self.n) if b.dim() != 2 else b
+        nrhs = b2.shape[0]
+        x = out if out is not None else torch.empty((nrhs, self.m), dtype=self.torch_dtype, device=self.device)
+        it = C.c_int32()
+        rn = (C.c_double * nrhs)()
+        an = (C.c_double * nrhs)()
+        self._stream()
+        _check(load_library().mht_lsqr(self._h, _dev_ptr(b2, self.n, nrhs, self.torch_dtype),
+                                       _dev_ptr(x, self.m, nrhs, self.torch_dtype), nrhs, int(max_iters),
+                                       float(atol), float(btol), C.byref(it), rn, an), "mht_lsqr")
+        return x, it.value, np.array(rn[:]), np.array(an[:])
 
     def apply_host(self, c_host: np.ndarray, f_host: np.ndarray | None = None):
         """End-to-end call from host memory (pinned for full bandwidth)."""

@@ -279,7 +279,7 @@ def test_split_k_small_blocks(gpu, oracle_lib, plans):
         Phi = rng.standard_normal((n, m))
         path = _dense_plan(plans, Phi, L, 1e-12, f"split_small_{n}_{m}_{L}")
         w = mi.Workload("sks", "mesh", n, m, "float64", 1e-12, L)
-        P, _ = check_plan(gpu, oracle_lib, path, w, (1, 2))
+        P, _ = check_plan(gpu, oracle_lib, path, w, (1, 2, 17, 64))
         c = torch.from_numpy(rng.standard_normal((1, m))).cuda()
         f1, f2 = P.apply(c), P.apply(c)
         assert torch.equal(f1, f2)
@@ -327,4 +327,89 @@ def test_persistent_matches_per_stage_launches(gpu, oracle_lib, plans):
         assert rel_cols(res[(True, True)][1].numpy(), O.adjoint(y)) <= PARITY
         P.set_persistent(True)
         P.set_fused_sums(True)
+        P.close()
+
+
+def test_multi_rhs_adjoint_k_split(gpu, oracle_lib, plans):
+    """Tall blocks on a low-parallelism stage take the multi-RHS adjoint K
+    split (row slabs summed in order by the last CTA): complex flat plan with
+    n >> m, parity vs O2 and the dense sums at several widths, and bitwise
+    determinism of repeated applies."""
+    path, w = flat_case(plans, 8192, 16, 2, 1e-10, name="tall")
+    P, _ = check_plan(gpu, oracle_lib, path, w, (2, 9, 32, 64), dense=flat_dense(oracle_lib, w))
+    y = torch.from_numpy(mi.complex_gaussian(40, w.n, 77)).cuda()
+    a1, a2 = P.adjoint(y), P.adjoint(y)
+    assert torch.equal(a1, a2)
+    P.close()
+
+
+def test_applications_fused_diagonal(gpu, oracle_lib, plans):
+    """PAPER.md §7: spectral filter f = Phi diag(F) c, filtered analysis
+    diag(d) Phi^* f, GRF sample y = Phi sqrt(S) z and covariance product
+    Phi S Phi^* v, each with the diagonal fused into the transform, against
+    the oracle's O2 applied to the explicitly scaled vectors (plain
+    definitions), at nrhs 1 and 5, complex and real plans, eager and graph."""
+    path_c, wc = flat_case(plans, 2048, 32, 4, 1e-8)
+    sp = str(plans / "sph_app.plan")
+    ws = W.sphere_workload(2048, 31, 4, 1e-10)
+    W.build_workload_plan(ws, sp, workers=8, log=None)
+    rng = np.random.default_rng(31)
+    for path, w in ((path_c, wc), (sp, ws)):
+        P = gpu.Plan(path)
+        O = oracle_lib.Plan(path)
+        lam = np.sort(rng.uniform(0, 100, w.m))
+        F = (lam < 40).astype(np.float64) + 0.5 * np.exp(-((lam - 70) / 10) ** 2)   # low-pass + bump (cf. Fig. 5)
+        S = (1.0 + lam) ** -1.5                                                     # Matern-like spectral density
+        Ft, St = torch.from_numpy(F).cuda(), torch.from_numpy(S).cuda()
+        for graphs in (True, False):
+            P.set_graphs(graphs)
+            for nrhs in (1, 5):
+                gen = mi.complex_gaussian if w.dtype == "complex128" else mi.real_gaussian
+                c, y = gen(nrhs, w.m, 500 + nrhs), gen(nrhs, w.n, 600 + nrhs)
+                ct, yt = torch.from_numpy(c).cuda(), torch.from_numpy(y).cuda()
+                assert rel_cols(P.apply_diag(ct, Ft).cpu().numpy(), O.apply(c * F[None, :])) <= PARITY
+                assert rel_cols(P.adjoint_diag(yt, Ft).cpu().numpy(), O.adjoint(y) * F[None, :]) <= PARITY
+                assert rel_cols(P.grf_sample(ct, St).cpu().numpy(), O.apply(c * np.sqrt(S)[None, :])) <= PARITY
+                cov = O.apply(O.adjoint(y) * S[None, :])
+                assert rel_cols(P.covariance_apply(yt, St).cpu().numpy(), cov) <= PARITY
+                # the plain transforms are unaffected afterwards (diagonal is per call)
+                assert rel_cols(P.apply(ct).cpu().numpy(), O.apply(c)) <= PARITY
+        P.close()
+
+
+def test_lsqr_inverse_mht(gpu, oracle_lib, plans):
+    """Inverse MHT by LSQR (§7.1, Eq. inverse-MHT): the GPU LSQR (plan
+    transforms + device vector kernels) follows the oracle's LSQR driven by
+    O2 iterate by iterate (atol = btol = 0, same k), and converges to the
+    dense least-squares solution; complex flat (n > m) and real mesh-like
+    (random dense Phi) plans, nrhs 1 and 3."""
+    from oracle.lsqr import lsqr_block
+
+    w = W.flat_workload(1024, 16, 2, 1e-12, name="lsqr_gpu")
+    path = str(plans / "lsqr_gpu.plan")
+    W.build_workload_plan(w, path, workers=8, log=None)
+    rng = np.random.default_rng(41)
+    Phi_r = rng.standard_normal((600, 150))
+    pr = _dense_plan(plans, Phi_r, 1, 1e-13, "lsqr_real")
+    wr = mi.Workload("lr", "mesh", 600, 150, "float64", 1e-13, 1)
+    x = mi.flat_points(w.n)
+    k = mi.flat_modes(16)
+    Phi_c = np.exp(1j * (x @ k.T.astype(float)))
+    for path_, w_, Phi in ((path, w, Phi_c), (pr, wr, Phi_r)):
+        P = gpu.Plan(path_)
+        O = oracle_lib.Plan(path_)
+        for nrhs in (1, 3):
+            gen = mi.complex_gaussian if w_.dtype == "complex128" else mi.real_gaussian
+            B = gen(nrhs, w_.n, 700 + nrhs)
+            Bt = torch.from_numpy(B).cuda()
+            for iters in (1, 4, 12):
+                X, it, rn, an = P.lsqr(Bt, iters)
+                assert it == iters
+                Xo, rno, ano = lsqr_block(lambda v: O.apply(v[None, :])[0], lambda u: O.adjoint(u[None, :])[0], B, iters)
+                assert rel_cols(X.cpu().numpy(), Xo) <= 1e-10, (path_, nrhs, iters)
+                assert np.allclose(rn, rno, rtol=1e-9, atol=0)
+            X, it, rn, an = P.lsqr(Bt, 400, atol=1e-12, btol=1e-12)
+            assert it < 400
+            Xs = np.linalg.lstsq(Phi, B.T, rcond=None)[0].T
+            assert rel_cols(X.cpu().numpy(), Xs) <= 1e-8, (path_, nrhs, it)
         P.close()
