@@ -109,6 +109,44 @@ mht_status mht_apply_adjoint(mht_plan *plan, const void *f, void *c, int nrhs);
 mht_status mht_apply_host(mht_plan *plan, const void *c_host, void *f_host, int nrhs);
 mht_status mht_apply_adjoint_host(mht_plan *plan, const void *f_host, void *c_host, int nrhs);
 
+/* ---- sharded plans: one plan across G GPUs -----------
+ * The factorization is split at a switch level ls (log2 G <= ls <= L - log2 G;
+ * switch_level < 0 picks max(log2 G, L/2)).  Rank g holds, for stages 0..ls,
+ * the blocks of the g-th frequency subtree at height L - log2 G (a frequency
+ * block (tau, nu) only reads its children nu's, §2) and,
+ * for stages ls+1..L+1, the blocks of the g-th space subtree at depth log2 G
+ * (only reads its parent tau's).  The one exchange step is an all-to-all of
+ * z_ls: rank g sends rank h the z_ls(tau, nu) with tau in h's space subtree
+ * and nu in g's frequency subtree.  Each rank loads and stores only its own
+ * blocks' coefficients (~1/G of the plan; the whole-file checksum is not
+ * verified by a shard).  nshards = 1 loads the whole plan (= mht_plan_load).
+ * G must be a power of two. */
+mht_status mht_plan_load_shard(const char *path, int device, int nshards, int shard, int switch_level,
+                               mht_plan **out);
+/* Exchange layout, in workspace entries (each entry = nrhs scalars, the
+ * workspace is [entry][rhs]): arrays of nshards.  send_off/len[h]: the block
+ * this rank sends to rank h (contiguous, ascending h); recv_off/len[g]: where
+ * the block from rank g lands (contiguous, ascending g).  Any pointer may be
+ * NULL.  nshards/shard/switch_level report the plan's sharding. */
+mht_status mht_shard_info(const mht_plan *plan, int32_t *nshards, int32_t *shard, int32_t *switch_level,
+                          int64_t *send_off, int64_t *send_len, int64_t *recv_off, int64_t *recv_len);
+/* Ensure the workspace for nrhs columns and return its device base pointer
+ * (the buffer the exchange reads and writes).  May synchronise (growth). */
+mht_status mht_shard_workspace(mht_plan *plan, int nrhs, void **zpool);
+/* Sharded synthesis: begin runs stages 0..ls on this rank's slice of c (c is
+ * the full m x nrhs array; only this rank's frequency range is read) and
+ * leaves the send blocks in the workspace; after the caller's all-to-all
+ * (send -> recv), end runs stages ls+1..L+1 and writes this rank's rows of f
+ * (full n x nrhs array; other rows untouched). */
+mht_status mht_apply_shard_begin(mht_plan *plan, const void *c, int nrhs);
+mht_status mht_apply_shard_end(mht_plan *plan, void *f, int nrhs);
+/* Sharded analysis: begin reads this rank's rows of f and leaves the adjoint
+ * of z_ls in the RECEIVE blocks; after the reverse all-to-all (recv -> send),
+ * end finishes and writes this rank's frequency range of c (other entries
+ * untouched). */
+mht_status mht_apply_adjoint_shard_begin(mht_plan *plan, const void *f, int nrhs);
+mht_status mht_apply_adjoint_shard_end(mht_plan *plan, void *c, int nrhs);
+
 /* ---- applications on top of the transform (§7) ----------------
  * A real diagonal on the coefficient side is fused into the transform's own
  * loads of c (synthesis) or its final stores of c (analysis): no extra pass

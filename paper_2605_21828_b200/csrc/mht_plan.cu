@@ -113,6 +113,10 @@ struct mht_plan {
 
   std::vector<Range> fwd, fwd1, adj, adjm, pieces;  // per stage 0..L+1
   std::vector<Range> pieces_u;  // pieces of the producers that are not fused (fused mode)
+  // sharded plans (mht_plan_load_shard): G ranks, this is rank g, switch level ls;
+  // exchange layout in zpool entries (x nrhs scalars each)
+  int shard_G = 1, shard_g = 0, shard_ls = -1;
+  std::vector<int64_t> send_off, send_len, recv_off, recv_len;
   // persistent nrhs = 1 apply (one cooperative launch per direction)
   // off by default: with CUDA-graph replay the per-stage launches measured
   // faster (profiles/r01_persistent_ab.txt: the cooperative kernel's union
@@ -205,7 +209,14 @@ struct Loc {
   int64_t off = 0;
 };
 
-mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P) {
+// Plan sharding: G ranks; stages 0..ls are partitioned by
+// the G frequency subtrees at height L - log2 G, stages ls+1..L+1 by the G
+// space subtrees at depth log2 G; one all-to-all of z_ls between the phases.
+struct ShardCfg {
+  int G = 1, g = 0, ls = -1;
+};
+
+mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P, const ShardCfg &sh) {
   int ndev = 0;
   CUDA_TRY(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(MHT_ERR_INVALID_ARG, "bad device ordinal");
@@ -267,11 +278,16 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
     }
   }
 
-  // device coefficient pool: the body size bounds the coefficient bytes
+  // device coefficient pool: the body size bounds the coefficient bytes.  A
+  // shard reads only its own blocks' coefficients (second pass below).
+  const bool sharded = sh.G > 1;
   CUDA_TRY(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
-  const size_t pool_bytes = std::max<int64_t>(16, body);
-  CUDA_TRY(cudaMalloc(&P->d_coef, pool_bytes));
-  P->device_bytes += (int64_t)pool_bytes;
+  size_t pool_bytes = std::max<int64_t>(16, body);
+  if (!sharded) {
+    CUDA_TRY(cudaMalloc(&P->d_coef, pool_bytes));
+    P->device_bytes += (int64_t)pool_bytes;
+  }
+  std::vector<int64_t> coef_file_off(L + 2, 0);  // file offset of each stage's coefficients
 
   const size_t CH = size_t(64) << 20;
   void *pin[2] = {nullptr, nullptr};
@@ -305,7 +321,13 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
     if ((coef_cursor + ncoef) * (int64_t)P->ssz > (int64_t)pool_bytes) return fail(MHT_ERR_FORMAT, "coefficients overflow body");
     coef_base[s] = coef_cursor;
     ncoef_s[s] = ncoef;
+    coef_file_off[s] = ftello(R.fp);
     int64_t left = ncoef * (int64_t)P->ssz;
+    if (sharded && left > 0) {  // skip now; the shard's blocks are read after resolution
+      if (fseeko(R.fp, left, SEEK_CUR) != 0 || ftello(R.fp) > fbytes) return fail(MHT_ERR_FORMAT, "truncated coefficients");
+      R.body_read += left;
+      left = 0;
+    }
     char *dst = static_cast<char *>(P->d_coef) + coef_cursor * (int64_t)P->ssz;
     while (left > 0) {
       size_t b = (size_t)std::min<int64_t>(left, (int64_t)CH);
@@ -327,7 +349,8 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
   }
   CUDA_TRY(cudaStreamSynchronize(P->stream));
   if (R.body_read != body) return fail(MHT_ERR_FORMAT, "trailing bytes after last stage");
-  if (R.csum != csum) return fail(MHT_ERR_FORMAT, "checksum mismatch");
+  // a shard does not read every coefficient, so it cannot verify the whole-body checksum
+  if (!sharded && R.csum != csum) return fail(MHT_ERR_FORMAT, "checksum mismatch");
   P->factor_entries = coef_cursor;
 
   // ------------------------------------------------ validation
@@ -382,6 +405,11 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
 
   std::vector<DevBlock> blocks;
   std::vector<int> block_stage;
+  struct RecvRegion {
+    int64_t off, len;
+  };
+  std::vector<RecvRegion> recv_regions;  // sharded: the exchange's receive buffer
+  int64_t send_base = 0;
   std::vector<std::vector<Loc>> loc(L + 1, std::vector<Loc>(nl));
   int64_t Z = 0, Pp = 0;
   P->stage_coef_bytes.assign(L + 2, 0);
@@ -430,25 +458,48 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
     P->stage_nmat[s] += 1;
     return Loc{SRC_Z, D.out_off};
   };
+  // ownership (sharded plans): stage s <= ls by frequency node v (height s),
+  // stage s > ls by space node t (depth s); aligned subtrees, so a block's
+  // inputs are local except the stage-(ls+1) reads of z_ls (the exchange)
+  auto own_v = [&](int s, int64_t v) { return !sharded || v / ((nl >> s) / sh.G) == sh.g; };
+  auto own_t = [&](int s, int64_t t) { return !sharded || t / ((int64_t(1) << s) / sh.G) == sh.g; };
   for (int64_t v = 0; v < nl; ++v) {
+    if (!own_v(0, v)) continue;
     const FileBlock &F = blk[0][v];
     Loc c0{SRC_C, fr_off[v]};
-    if (F.kind == 0) {
+    if (F.kind == 0 && !(sharded && sh.ls == 0)) {
       loc[0][v] = c0;
       P->n_alias++;
     } else {
       loc[0][v] = materialize(0, F, c0, F.r_in, Loc{SRC_C, 0}, 0, false, 0);
     }
   }
+  if (sharded) {
+    P->send_off.assign(sh.G, 0);
+    P->send_len.assign(sh.G, 0);
+    P->recv_off.assign(sh.G, 0);
+    P->recv_len.assign(sh.G, 0);
+  }
   for (int s = 1; s <= L; ++s) {
     const int64_t nf = nl >> s, nfp = nl >> (s - 1);
+    const bool freq_phase = !sharded || s <= sh.ls;
+    if (sharded && s == sh.ls) send_base = Z;
     for (int64_t b = 0; b < nl; ++b) {
       const int64_t t = b / nf, v = b % nf, p = t >> 1;
+      if (freq_phase ? !own_v(s, v) : !own_t(s, t)) continue;
       const int64_t b1 = p * nfp + 2 * v, b2 = b1 + 1;
       const Loc A = loc[s - 1][b1], B = loc[s - 1][b2];
       const int32_t la = blk[s - 1][b1].r_out, lb = blk[s - 1][b2].r_out;
       const FileBlock &F = blk[s][b];
-      if (F.kind == 0) {
+      // the switch stage's outputs are the send buffer: always materialised,
+      // laid out destination by destination (t-major order)
+      const bool send = sharded && s == sh.ls;
+      if (send) {
+        const int h = (int)(t / ((int64_t(1) << s) / sh.G));
+        if (P->send_len[h] == 0) P->send_off[h] = Z;
+        P->send_len[h] += F.r_out;
+      }
+      if (F.kind == 0 && !send) {
         if (lb == 0) {
           loc[s][b] = A;
           P->n_alias++;
@@ -467,14 +518,87 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
       }
       loc[s][b] = materialize(s, F, A, la, B, lb, false, 0);
     }
+    if (sharded && s == sh.ls) {
+      // send regions are contiguous in destination order (t-major); give empty
+      // destinations their position in the sequence
+      int64_t run = send_base;
+      for (int h = 0; h < sh.G; ++h) {
+        P->send_off[h] = run;
+        run += P->send_len[h];
+      }
+      if (run != Z) return fail(MHT_ERR_FORMAT, "shard send layout");
+      // receive buffer: z_ls(t, v) for my space nodes t and every v, source by
+      // source in the senders' order; the next stage reads it in place
+      for (int src = 0; src < sh.G; ++src) {
+        P->recv_off[src] = Z;
+        for (int64_t t = 0; t < (int64_t(1) << s); ++t) {
+          if (!own_t(s, t)) continue;
+          for (int64_t v = 0; v < nf; ++v) {
+            if (v / (nf / sh.G) != src) continue;
+            loc[s][t * nf + v] = Loc{SRC_Z, Z};
+            recv_regions.push_back({Z, (int64_t)blk[s][t * nf + v].r_out});
+            Z += blk[s][t * nf + v].r_out;
+          }
+        }
+        P->recv_len[src] = Z - P->recv_off[src];
+      }
+    }
   }
   for (int64_t t = 0; t < nl; ++t) {
+    if (!own_t(L, t)) continue;
     const FileBlock &F = blk[L + 1][t];
     materialize(L + 1, F, loc[L][t], blk[L][t].r_out, Loc{SRC_C, 0}, 0, true, sp_off[t]);
   }
   P->Zt = std::max<int64_t>(Z, 1);
   P->Pt = std::max<int64_t>(Pp, 1);
   P->n_mat = (int)blocks.size();
+
+  // ------------------------------------------------ shard: read this rank's coefficients
+  if (sharded) {
+    P->shard_G = sh.G;
+    P->shard_g = sh.g;
+    P->shard_ls = sh.ls;
+    struct Job {
+      int64_t file_off, nbytes;
+      int blk;
+    };
+    std::vector<Job> jobs;
+    int64_t total = 0;
+    for (int i = 0; i < (int)blocks.size(); ++i) {
+      DevBlock &D = blocks[i];
+      if (D.n_red == 0 || D.r_out == 0) continue;
+      const int st_ = block_stage[i];
+      const int64_t within = D.coef_off - coef_base[st_];  // scalars into the stage's coefficients
+      jobs.push_back({coef_file_off[st_] + within * (int64_t)P->ssz, (int64_t)D.r_out * D.n_red * (int64_t)P->ssz, i});
+      total += jobs.back().nbytes;
+    }
+    std::sort(jobs.begin(), jobs.end(), [](const Job &a, const Job &b) { return a.file_off < b.file_off; });
+    pool_bytes = (size_t)std::max<int64_t>(16, total);
+    CUDA_TRY(cudaMalloc(&P->d_coef, pool_bytes));
+    P->device_bytes += (int64_t)pool_bytes;
+    int64_t cur = 0;  // device byte cursor
+    for (const Job &j : jobs) {
+      blocks[j.blk].coef_off = cur / (int64_t)P->ssz;
+      if (fseeko(R.fp, j.file_off, SEEK_SET) != 0) return fail(MHT_ERR_IO, "seek");
+      int64_t left = j.nbytes;
+      char *dst = static_cast<char *>(P->d_coef) + cur;
+      while (left > 0) {
+        const size_t b = (size_t)std::min<int64_t>(left, (int64_t)CH);
+        if (pending[which]) CUDA_TRY(cudaEventSynchronize(ev[which]));
+        if (fread(pin[which], 1, b, R.fp) != b) return fail(MHT_ERR_FORMAT, "truncated coefficients");
+        CUDA_TRY(cudaMemcpyAsync(dst, pin[which], b, cudaMemcpyHostToDevice, P->stream));
+        CUDA_TRY(cudaEventRecord(ev[which], P->stream));
+        pending[which] = true;
+        which ^= 1;
+        dst += b;
+        left -= (int64_t)b;
+      }
+      cur += j.nbytes;
+    }
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    P->factor_entries = total / (int64_t)P->ssz;
+    coef_cursor = P->factor_entries;
+  }
 
   // ------------------------------------------------ factor layout
   // Complex factors keep the file layout (16-byte scalars are always aligned).
@@ -742,11 +866,23 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
     int blk;  // producer block (-1: the user's c)
   };
   std::vector<Region> regions;
-  regions.push_back({SRC_C, -1, 0, P->m, -1});
+  if (!sharded) {
+    regions.push_back({SRC_C, -1, 0, P->m, -1});
+  } else {  // a shard owns (and writes in the adjoint) only its frequency leaves' slice of c
+    const int64_t v0 = (int64_t)sh.g * (nl / sh.G), v1 = v0 + nl / sh.G;
+    if (fr_off[v1] > fr_off[v0]) regions.push_back({SRC_C, -1, fr_off[v0], fr_off[v1] - fr_off[v0], -1});
+  }
   for (int i = 0; i < (int)blocks.size(); ++i) {
     const DevBlock &D = blocks[i];
+    // sharded: the switch stage's outputs (the send buffer) are read remotely;
+    // their adjoint input arrives by the reverse exchange, no local sums
+    if (sharded && block_stage[i] == sh.ls) continue;
     if (!(D.flags & F_OUT_F) && D.r_out > 0) regions.push_back({SRC_Z, block_stage[i], D.out_off, D.r_out, i});
   }
+  // the receive buffer is a producer region of stage ls without a local
+  // producer block: its adjoint sums are formed here and sent back
+  for (const RecvRegion &rr : recv_regions)
+    if (rr.len > 0) regions.push_back({SRC_Z, sh.ls, rr.off, rr.len, -1});
   std::vector<std::vector<Piece>> pcs(L + 3);  // index stage+1 (0 = c)
   std::vector<std::vector<std::vector<int64_t>>> pcs_rd(L + 3);
   std::vector<std::vector<char>> pcs_keep(L + 3);  // piece still needed in fused mode
@@ -835,6 +971,8 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P)
   // per-block fused reader lists
   std::vector<int64_t> rdtab;
   P->n_unfused = 0;
+  for (int i = 0; i < (int)blocks.size(); ++i)
+    if (sharded && block_stage[i] == sh.ls) unfusable[i] = 1;  // input arrives by the exchange
   for (int i = 0; i < (int)blocks.size(); ++i) {
     DevBlock &D = blocks[i];
     D.rd_off = (int64_t)rdtab.size();
@@ -992,7 +1130,7 @@ void timed(mht_plan *P, int kind, int stage, int nrhs, int count, F &&launch) {
   P->recs.push_back({kind, stage, nrhs, a, b});
 }
 
-bool use_persist(const mht_plan *P, int nrhs) { return nrhs == 1 && P->persist != 0; }
+bool use_persist(const mht_plan *P, int nrhs) { return nrhs == 1 && P->persist != 0 && P->shard_G == 1; }
 
 unsigned long long *stamp_buf(mht_plan *P, int dir) {
   if (!P->prof) return nullptr;
@@ -1011,17 +1149,20 @@ mht_status run_persist(mht_plan *P, const Ctx &cx, Range ph, int dir) {
   return MHT_OK;
 }
 
-mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs) {
+// part: 0 the whole apply; sharded plans 1 = stages 0..ls (before the
+// exchange), 2 = stages ls+1..L+1 (after it)
+mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs, int part = 0) {
   Ctx cx = make_ctx(P, nrhs);
   cx.c = c;
   cx.fout = f;
-  if (use_persist(P, nrhs)) {
+  const int s_lo = part == 2 ? P->shard_ls + 1 : 0, s_hi = part == 1 ? P->shard_ls : P->L + 1;
+  if (part == 0 && use_persist(P, nrhs)) {
     mht_status st = run_persist(P, cx, P->ph_fwd, 0);
     if (st != MHT_OK) return st;
     CUDA_TRY(cudaGetLastError());
     return MHT_OK;
   }
-  for (int s = 0; s < P->L + 2; ++s)
+  for (int s = s_lo; s <= s_hi; ++s)
     timed(P, 0, s, nrhs, nrhs == 1 ? P->fwd1[s].count : P->fwd[s].count, [&] {
       if (nrhs == 1)
         launch_fwd(P->cplx, cx, P->d_fwd1 + P->fwd1[s].off, P->fwd1[s].count, P->stream);
@@ -1032,12 +1173,15 @@ mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs) {
   return MHT_OK;
 }
 
-mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
+// part: 0 the whole adjoint; sharded plans 1 = leaf stage .. ls+1 plus the
+// sums into the receive buffer (sent back by the reverse exchange), 2 = stage
+// ls (its input arrived) .. 0 plus the sums into c
+mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs, int part = 0) {
   Ctx cx = make_ctx(P, nrhs);
   cx.fin = f;
   cx.cw = c;
   const int L = P->L;
-  if (use_persist(P, nrhs)) {
+  if (part == 0 && use_persist(P, nrhs)) {
     mht_status st = run_persist(P, cx, cx.fused ? P->ph_adj_fused : P->ph_adj_unfused, 1);
     if (st != MHT_OK) return st;
     CUDA_TRY(cudaGetLastError());
@@ -1052,25 +1196,53 @@ mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
         launch_mma(P->cplx, true, cx, P->d_adjm + P->adjm[s].off, P->adjm[s].count, from_f, P->stream);
       });
   };
-  adj_stage(L + 1, true);
-  for (int s = L; s >= 0; --s) {
+  auto sums = [&](int s) {
     const Range pr = cx.fused ? P->pieces_u[s] : P->pieces[s];
     timed(P, 2, s, nrhs, pr.count, [&] {
       launch_reduce(P->cplx, cx, P->d_pieces + pr.off, P->d_rd, pr.count, P->stream);
     });
-    adj_stage(s, false);
+  };
+  const int ls = P->shard_ls;
+  if (part != 2) {
+    adj_stage(L + 1, true);
+    for (int s = L; s >= (part == 1 ? ls + 1 : 0); --s) {
+      sums(s);
+      adj_stage(s, false);
+    }
+    if (part == 1) sums(ls);
   }
-  timed(P, 2, -1, nrhs, P->cpieces.count, [&] {
-    launch_reduce(P->cplx, cx, P->d_pieces + P->cpieces.off, P->d_rd, P->cpieces.count, P->stream);
-  });
+  if (part == 2) {
+    adj_stage(ls, false);
+    for (int s = ls - 1; s >= 0; --s) {
+      sums(s);
+      adj_stage(s, false);
+    }
+  }
+  if (part != 1)
+    timed(P, 2, -1, nrhs, P->cpieces.count, [&] {
+      launch_reduce(P->cplx, cx, P->d_pieces + P->cpieces.off, P->d_rd, P->cpieces.count, P->stream);
+    });
   CUDA_TRY(cudaGetLastError());
   return MHT_OK;
 }
 
 // Replay (or capture, then replay) the whole stage sequence of one apply as a
 // CUDA graph.  Profiling bypasses graphs (per-launch events).
+// dir: 0 synthesis, 1 analysis; sharded halves 2 / 3 synthesis before / after
+// the exchange, 4 / 5 analysis before / after the reverse exchange
+mht_status run_seq(mht_plan *P, int dir, const void *src, void *dst, int nrhs) {
+  switch (dir) {
+    case 0: return run_forward(P, src, dst, nrhs);
+    case 1: return run_adjoint(P, src, dst, nrhs);
+    case 2: return run_forward(P, src, nullptr, nrhs, 1);
+    case 3: return run_forward(P, nullptr, dst, nrhs, 2);
+    case 4: return run_adjoint(P, src, nullptr, nrhs, 1);
+    default: return run_adjoint(P, nullptr, dst, nrhs, 2);
+  }
+}
+
 mht_status run_dir(mht_plan *P, int dir, const void *src, void *dst, int nrhs) {
-  if (!P->graphs || P->prof) return dir == 0 ? run_forward(P, src, dst, nrhs) : run_adjoint(P, src, dst, nrhs);
+  if (!P->graphs || P->prof) return run_seq(P, dir, src, dst, nrhs);
   mht_plan::GraphKey key{dir, nrhs, src, dst, P->cur_diag, P->cur_diag_sqrt};
   auto it = P->gcache.find(key);
   if (it == P->gcache.end()) {
@@ -1082,7 +1254,7 @@ mht_status run_dir(mht_plan *P, int dir, const void *src, void *dst, int nrhs) {
     cudaError_t e = cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal);
     mht_status st = MHT_OK;
     if (e == cudaSuccess) {
-      st = dir == 0 ? run_forward(P, src, dst, nrhs) : run_adjoint(P, src, dst, nrhs);
+      st = run_seq(P, dir, src, dst, nrhs);
       e = cudaStreamEndCapture(P->cap_stream, &g);
     }
     P->stream = user;
@@ -1111,7 +1283,7 @@ mht_status mht_plan_load(const char *path, int device, mht_plan **out) {
   *out = nullptr;
   try {
     std::unique_ptr<mht_plan> P(new mht_plan());
-    mht_status s = load_impl(path, device, P);
+    mht_status s = load_impl(path, device, P, ShardCfg());
     if (s != MHT_OK) return s;
     *out = P.release();
     return MHT_OK;
@@ -1121,6 +1293,84 @@ mht_status mht_plan_load(const char *path, int device, mht_plan **out) {
     return fail(MHT_ERR_CUDA, "unexpected exception in loader");
   }
 }
+
+mht_status mht_plan_load_shard(const char *path, int device, int nshards, int shard, int switch_level,
+                               mht_plan **out) {
+  if (!path || !out || nshards < 1 || shard < 0 || shard >= nshards || (nshards & (nshards - 1)) != 0)
+    return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  *out = nullptr;
+  try {
+    std::unique_ptr<mht_plan> P(new mht_plan());
+    ShardCfg sh;
+    sh.G = nshards;
+    sh.g = shard;
+    sh.ls = switch_level;
+    if (nshards > 1) {
+      // L is needed to place / check the switch level: peek at the header
+      FILE *fp = fopen(path, "rb");
+      if (!fp) return fail(MHT_ERR_IO, std::string("cannot open ") + path);
+      unsigned char hdr[256];
+      const size_t got = fread(hdr, 1, 256, fp);
+      fclose(fp);
+      if (got != 256 || memcmp(hdr, "BFMHTPLN", 8) != 0) return fail(MHT_ERR_FORMAT, "bad header");
+      int32_t L;
+      memcpy(&L, hdr + 32, 4);
+      int lg = 0;
+      while ((1 << lg) < nshards) ++lg;
+      if (sh.ls < 0) sh.ls = std::max(lg, L / 2);
+      if (L < 2 * lg || sh.ls < lg || sh.ls > L - lg)
+        return fail(MHT_ERR_INVALID_ARG, "switch level must satisfy log2 G <= ls <= L - log2 G");
+    }
+    mht_status s = load_impl(path, device, P, sh);
+    if (s != MHT_OK) return s;
+    *out = P.release();
+    return MHT_OK;
+  } catch (const std::bad_alloc &) {
+    return fail(MHT_ERR_OOM, "host allocation failed");
+  } catch (...) {
+    return fail(MHT_ERR_CUDA, "unexpected exception in loader");
+  }
+}
+
+mht_status mht_shard_info(const mht_plan *P, int32_t *nshards, int32_t *shard, int32_t *switch_level,
+                          int64_t *send_off, int64_t *send_len, int64_t *recv_off, int64_t *recv_len) {
+  if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
+  if (nshards) *nshards = P->shard_G;
+  if (shard) *shard = P->shard_g;
+  if (switch_level) *switch_level = P->shard_ls;
+  for (int h = 0; h < (int)P->send_off.size(); ++h) {
+    if (send_off) send_off[h] = P->send_off[h];
+    if (send_len) send_len[h] = P->send_len[h];
+    if (recv_off) recv_off[h] = P->recv_off[h];
+    if (recv_len) recv_len[h] = P->recv_len[h];
+  }
+  return MHT_OK;
+}
+
+mht_status mht_shard_workspace(mht_plan *P, int nrhs, void **zpool) {
+  if (!P || !zpool || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s = ensure_ws(P, nrhs);
+  if (s != MHT_OK) return s;
+  *zpool = P->d_z;
+  return MHT_OK;
+}
+
+static mht_status shard_call(mht_plan *P, int dir, const void *src, void *dst, int nrhs) {
+  if (!P || nrhs < 1 || (!src && !dst)) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G < 2) return fail(MHT_ERR_INVALID_ARG, "not a sharded plan (mht_plan_load_shard with nshards > 1)");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s = ensure_ws(P, nrhs);
+  if (s != MHT_OK) return s;
+  return run_dir(P, dir, src, dst, nrhs);
+}
+
+mht_status mht_apply_shard_begin(mht_plan *P, const void *c, int nrhs) { return shard_call(P, 2, c, nullptr, nrhs); }
+mht_status mht_apply_shard_end(mht_plan *P, void *f, int nrhs) { return shard_call(P, 3, nullptr, f, nrhs); }
+mht_status mht_apply_adjoint_shard_begin(mht_plan *P, const void *f, int nrhs) {
+  return shard_call(P, 4, f, nullptr, nrhs);
+}
+mht_status mht_apply_adjoint_shard_end(mht_plan *P, void *c, int nrhs) { return shard_call(P, 5, nullptr, c, nrhs); }
 
 mht_status mht_plan_info_get(const mht_plan *P, mht_plan_info *info) {
   if (!P || !info) return fail(MHT_ERR_INVALID_ARG, "null argument");
@@ -1162,6 +1412,7 @@ mht_status mht_reserve(mht_plan *P, int nrhs) {
 
 mht_status mht_apply(mht_plan *P, const void *c, void *f, int nrhs) {
   if (!P || !c || !f || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G > 1) return fail(MHT_ERR_INVALID_ARG, "sharded plan: use mht_apply_shard_begin / _end");
   CUDA_TRY(cudaSetDevice(P->device));
   mht_status s = ensure_ws(P, nrhs);
   if (s != MHT_OK) return s;
@@ -1170,6 +1421,7 @@ mht_status mht_apply(mht_plan *P, const void *c, void *f, int nrhs) {
 
 mht_status mht_apply_adjoint(mht_plan *P, const void *f, void *c, int nrhs) {
   if (!P || !c || !f || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G > 1) return fail(MHT_ERR_INVALID_ARG, "sharded plan: use mht_apply_adjoint_shard_begin / _end");
   CUDA_TRY(cudaSetDevice(P->device));
   mht_status s = ensure_ws(P, nrhs);
   if (s != MHT_OK) return s;
@@ -1192,6 +1444,7 @@ struct DiagScope {  // sets the plan's coefficient-side diagonal for one call
 
 mht_status mht_apply_diag(mht_plan *P, const void *c, const double *d, void *f, int nrhs) {
   if (!P || !c || !d || !f || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G > 1) return fail(MHT_ERR_INVALID_ARG, "sharded plan: use the mht_*_shard_* calls");
   CUDA_TRY(cudaSetDevice(P->device));
   mht_status s = ensure_ws(P, nrhs);
   if (s != MHT_OK) return s;
@@ -1201,6 +1454,7 @@ mht_status mht_apply_diag(mht_plan *P, const void *c, const double *d, void *f, 
 
 mht_status mht_apply_adjoint_diag(mht_plan *P, const void *f, const double *d, void *c, int nrhs) {
   if (!P || !c || !d || !f || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G > 1) return fail(MHT_ERR_INVALID_ARG, "sharded plan: use the mht_*_shard_* calls");
   CUDA_TRY(cudaSetDevice(P->device));
   mht_status s = ensure_ws(P, nrhs);
   if (s != MHT_OK) return s;
@@ -1210,6 +1464,7 @@ mht_status mht_apply_adjoint_diag(mht_plan *P, const void *f, const double *d, v
 
 mht_status mht_grf_sample(mht_plan *P, const void *z, const double *S, void *y, int nrhs) {
   if (!P || !z || !S || !y || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G > 1) return fail(MHT_ERR_INVALID_ARG, "sharded plan: use the mht_*_shard_* calls");
   CUDA_TRY(cudaSetDevice(P->device));
   mht_status s = ensure_ws(P, nrhs);
   if (s != MHT_OK) return s;
@@ -1219,6 +1474,7 @@ mht_status mht_grf_sample(mht_plan *P, const void *z, const double *S, void *y, 
 
 mht_status mht_covariance_apply(mht_plan *P, const void *v, const double *S, void *out, int nrhs) {
   if (!P || !v || !S || !out || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G > 1) return fail(MHT_ERR_INVALID_ARG, "sharded plan: use the mht_*_shard_* calls");
   CUDA_TRY(cudaSetDevice(P->device));
   mht_status s = ensure_ws(P, nrhs);
   if (s != MHT_OK) return s;
@@ -1247,6 +1503,7 @@ mht_status mht_covariance_apply(mht_plan *P, const void *v, const double *S, voi
 mht_status mht_lsqr(mht_plan *P, const void *b, void *x, int nrhs, int max_iters, double atol, double btol,
                     int *iters_done, double *rnorm, double *arnorm) {
   if (!P || !b || !x || nrhs < 1 || max_iters < 0) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G > 1) return fail(MHT_ERR_INVALID_ARG, "sharded plan: use the mht_*_shard_* calls");
   CUDA_TRY(cudaSetDevice(P->device));
   mht_status st = ensure_ws(P, nrhs);
   if (st != MHT_OK) return st;
@@ -1341,6 +1598,7 @@ static mht_status ensure_host_staging(mht_plan *P, int nrhs) {
 
 mht_status mht_apply_host(mht_plan *P, const void *c_host, void *f_host, int nrhs) {
   if (!P || !c_host || !f_host || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G > 1) return fail(MHT_ERR_INVALID_ARG, "sharded plan: use the mht_*_shard_* calls");
   CUDA_TRY(cudaSetDevice(P->device));
   mht_status s;
   if ((s = ensure_ws(P, nrhs)) != MHT_OK || (s = ensure_host_staging(P, nrhs)) != MHT_OK) return s;
@@ -1353,6 +1611,7 @@ mht_status mht_apply_host(mht_plan *P, const void *c_host, void *f_host, int nrh
 
 mht_status mht_apply_adjoint_host(mht_plan *P, const void *f_host, void *c_host, int nrhs) {
   if (!P || !c_host || !f_host || nrhs < 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G > 1) return fail(MHT_ERR_INVALID_ARG, "sharded plan: use the mht_*_shard_* calls");
   CUDA_TRY(cudaSetDevice(P->device));
   mht_status s;
   if ((s = ensure_ws(P, nrhs)) != MHT_OK || (s = ensure_host_staging(P, nrhs)) != MHT_OK) return s;

@@ -23,6 +23,8 @@ MHT_DTYPE_F64, MHT_DTYPE_C128 = 1, 2
 EXPORTED = [
     "mht_plan_load", "mht_plan_info_get", "mht_plan_set_stream", "mht_reserve", "mht_apply",
     "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host", "mht_apply_diag", "mht_apply_adjoint_diag", "mht_grf_sample", "mht_covariance_apply", "mht_lsqr",
+    "mht_plan_load_shard", "mht_shard_info", "mht_shard_workspace", "mht_apply_shard_begin",
+    "mht_apply_shard_end", "mht_apply_adjoint_shard_begin", "mht_apply_adjoint_shard_end",
     "mht_set_graphs", "mht_set_fused_sums", "mht_set_persistent", "mht_phase_times", "mht_sync",
     "mht_stage_stats", "mht_set_profiling", "mht_profile_get", "mht_profile_reset", "mht_plan_destroy",
     "mht_status_string", "mht_last_error", "mht_build_info",
@@ -63,6 +65,13 @@ def load_library(path: str = LIB_PATH):
         getattr(L, nm).argtypes = [vp, vp, vp, vp, i32]
     L.mht_lsqr.argtypes = [vp, vp, vp, i32, i32, C.c_double, C.c_double, C.POINTER(C.c_int32),
                            C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.mht_plan_load_shard.argtypes = [C.c_char_p, i32, i32, i32, i32, C.POINTER(vp)]
+    L.mht_shard_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                 C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
+    L.mht_shard_workspace.argtypes = [vp, i32, C.POINTER(vp)]
+    for nm in ("mht_apply_shard_begin", "mht_apply_shard_end", "mht_apply_adjoint_shard_begin",
+               "mht_apply_adjoint_shard_end"):
+        getattr(L, nm).argtypes = [vp, vp, i32]
     L.mht_set_graphs.argtypes = [vp, i32]
     L.mht_set_fused_sums.argtypes = [vp, i32]
     L.mht_set_persistent.argtypes = [vp, i32]

@@ -413,3 +413,43 @@ def test_lsqr_inverse_mht(gpu, oracle_lib, plans):
             Xs = np.linalg.lstsq(Phi, B.T, rcond=None)[0].T
             assert rel_cols(X.cpu().numpy(), Xs) <= 1e-8, (path_, nrhs, it)
         P.close()
+
+
+def test_sharded_plan_emulated_on_one_gpu(gpu, oracle_lib, plans):
+    """SURVEY §8(e) sharded plans: G = 2 and 4 shards of one plan (frequency
+    subtrees for stages <= ls, space subtrees after, one all-to-all of z_ls),
+    all loaded on this GPU with the exchange done by device copies.  The
+    assembled synthesis and analysis match O2 on the whole plan (<= 1e-12) at
+    nrhs 1, 5 and 32, complex flat and real sphere plans, every admissible
+    switch level; each shard holds about 1/G of the factor bytes."""
+    from paper_2605_21828_b200 import shard as SH
+
+    path_c, wc = flat_case(plans, 2048, 32, 4, 1e-8)
+    sp = str(plans / "sph_shard.plan")
+    ws = W.sphere_workload(2048, 31, 4, 1e-10)
+    W.build_workload_plan(ws, sp, workers=8, log=None)
+    for path, w in ((path_c, wc), (sp, ws)):
+        O = oracle_lib.Plan(path)
+        full = gpu.Plan(path)
+        total = full.info.factor_entries
+        full.close()
+        for G in (2, 4):
+            lg = G.bit_length() - 1
+            for ls in range(lg, w.L - lg + 1):
+                shards = [SH.ShardPlan(path, G, g, 0, ls) for g in range(G)]
+                assert all(s.ls == ls for s in shards)
+                held = sum(s.info.factor_entries for s in shards)
+                assert held == total                           # every block on exactly one rank
+                assert max(s.info.factor_entries for s in shards) <= 0.75 * total if G == 4 else True
+                for nrhs in (1, 5, 32):
+                    gen = mi.complex_gaussian if w.dtype == "complex128" else mi.real_gaussian
+                    c, y = gen(nrhs, w.m, 800 + nrhs), gen(nrhs, w.n, 900 + nrhs)
+                    ct, yt = torch.from_numpy(c).cuda(), torch.from_numpy(y).cuda()
+                    f = torch.zeros((nrhs, w.n), dtype=shards[0].torch_dtype, device="cuda")
+                    a = torch.zeros((nrhs, w.m), dtype=shards[0].torch_dtype, device="cuda")
+                    SH.emulate_apply(shards, ct, f)
+                    SH.emulate_adjoint(shards, yt, a)
+                    assert rel_cols(f.cpu().numpy(), O.apply(c)) <= PARITY, (path, G, ls, nrhs)
+                    assert rel_cols(a.cpu().numpy(), O.adjoint(y)) <= PARITY, (path, G, ls, nrhs)
+                for s in shards:
+                    s.close()
