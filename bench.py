@@ -54,6 +54,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "shard"],
+                    help="replicas (default): every rank holds the whole plan and transforms its own columns "
+                         "(weak scaling, no data-path collective); shard: the plan is split across the ranks "
+                         "and every transform is done jointly with one NCCL all-to-all (strong scaling)")
     ap.add_argument("--cpu-table", action="store_true",
                     help="cpu_baseline leg only: time the oracle (O2 at 1 and all threads, O1 dense sum full or on "
                          "a labelled row subset) on this host for --workload, print one JSON line, exit")
@@ -287,6 +291,8 @@ def main():
             run_reference(args, w, get_plan(w, args, 1, rank, lrank))
         return
     path = get_plan(w, args, ws, rank, lrank)
+    if args.mode == "shard" and ws > 1:
+        return run_shard(args, w, path, ws, rank, lrank)
 
     from paper_2605_21828_b200 import mht, replicas
 
@@ -453,6 +459,70 @@ def main():
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def run_shard(args, w, path, ws, rank, lrank):
+    """--mode shard under torchrun: rank g holds shard g of the plan (frequency
+    subtrees up to the switch level, space subtrees after it; DESIGN.md §7);
+    every transform of the step is done jointly by all ranks, the exchange is
+    one torch.distributed (NCCL) all_to_all_single of z_ls per direction."""
+    import torch
+
+    from paper_2605_21828_b200 import replicas
+    from paper_2605_21828_b200 import shard as SH
+
+    dev = torch.device("cuda", lrank)
+    S = SH.ShardPlan(path, ws, rank, lrank)
+    phases = phases_for(w)
+    ins, outs = {}, {}
+    for kind, r in phases:
+        if kind == "fwd":
+            ins[(kind, r)] = torch.from_numpy(mi.workload_coefficients(w, r)).to(dev)
+            outs[(kind, r)] = torch.zeros((r, w.n), dtype=S.torch_dtype, device=dev)
+        else:
+            ins[(kind, r)] = torch.from_numpy(mi.workload_adjoint_input(w, r)).to(dev)
+            outs[(kind, r)] = torch.zeros((r, w.m), dtype=S.torch_dtype, device=dev)
+
+    def step():
+        for kind, r in phases:
+            if kind == "fwd":
+                S.apply(ins[(kind, r)], outs[(kind, r)])
+            else:
+                S.adjoint(ins[(kind, r)], outs[(kind, r)])
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(lrank)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier(ws)
+    torch.cuda.synchronize()
+    clocks.start()
+    for k in range(args.steps):
+        ev[k][0].record()
+        step()
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier(ws)
+    total_ms = allreduce_max(sum(a.elapsed_time(b) for a, b in ev), ws)
+    transforms = sum(r for _, r in phases)
+    exch = int(sum(S.send_len) - S.send_len[rank])  # entries this rank sends per RHS column and direction
+    out = {"metric": METRIC, "value": transforms * args.steps / (total_ms / 1e3), "unit": UNIT, "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype_tag(w),
+           "data": "synthetic (seeded generators in mht_inputs; no paper dataset)",
+           "config": {"workload": workload_desc(w), "phases": [f"{k}@nrhs{r}" for k, r in phases],
+                      "transforms_per_step": transforms, "parallelism": f"shard{ws} (switch level {S.ls})",
+                      "factor_entries_this_rank": S.info.factor_entries,
+                      "exchange_bytes_per_rhs_per_direction_this_rank": exch * S.scalar_bytes},
+           "clocks": clk, "gpu_launches": None}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    S.close()
+    import torch.distributed as dist
+
+    dist.destroy_process_group()
 
 
 def _e2e(P, phases, w, ws, args):
