@@ -460,6 +460,100 @@ struct Planes<double2> {
 // M3: complex products by Gauss's 3-multiplication form (P1 = Ar Br, P2 = Ai Bi,
 // P3 = (Ar + Ai)(Br + Bi); re = P1 - P2, im = P3 - P1 - P2) — 3 DMMAs instead of 4.
 // MINB: CTAs per SM the register budget is sized for.
+// barrier over the 128 consumer threads: __syncthreads (BAR = 0) in the
+// classic kernel, named barrier 1 in the warp-specialised one (its producer
+// warp does not take part in the epilogue)
+template <int BAR>
+__device__ __forceinline__ void consumer_sync() {
+  if constexpr (BAR == 0)
+    __syncthreads();
+  else
+    asm volatile("bar.sync 1, %0;" ::"n"(MM_THREADS) : "memory");
+}
+
+// Multi-RHS epilogue (threads 0..127): C fragments (row gid / gid + 8, cols
+// 2 tig / 2 tig + 1) -> skeleton add and the output store (forward), partials
+// (adjoint) or the K-split slabs with the last-CTA fixup.
+template <class S, bool ADJ, int NT, bool M3, int BAR>
+__device__ __forceinline__ void mma_epilogue(const Ctx &cx, const Tile &tl, const DevBlock &B, double (&c0)[NT][4],
+                                             double (&c1)[NT][4], double (&c2)[(Planes<S>::cplx && M3) ? NT : 1][4],
+                                             int rhs0, bool ksplit, int sidx, int from_f, int *flag) {
+  using X = Tr<S>;
+  constexpr bool CPLX = Planes<S>::cplx;
+  constexpr bool G3 = CPLX && M3;
+  constexpr int NRT = 8 * NT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const bool red_iota = (B.flags & F_RED_IOTA) != 0;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int m = warp * 16 + gid + 8 * (v >> 1);
+      const int r = rhs0 + t * 8 + 2 * tig + (v & 1);
+      if (m >= tl.count || r >= cx.nrhs) continue;
+      S val;
+      if constexpr (!CPLX) {
+        val = c0[t][v];
+      } else if constexpr (G3) {
+        val = make_double2(c0[t][v] - c1[t][v], c2[t][v] - c0[t][v] - c1[t][v]);
+      } else {
+        val = make_double2(c0[t][v], c1[t][v]);
+      }
+      const int row = tl.start + m;
+      if (!ADJ) {
+        if (row < B.n_skel) {
+          const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
+          val = X::add(val, in_value<S>(cx, B, q, r));
+        }
+        if (B.flags & F_OUT_F)
+          static_cast<S *>(cx.fout)[r * cx.n + cx.perm[B.out_off + row]] = val;
+        else
+          static_cast<S *>(cx.z)[(B.out_off + row) * cx.nrhs + r] = val;
+      } else if (ksplit) {
+        const int64_t slab = B.msp_off + (int64_t)(tl.start / MMA_COLS) * B.mks + sidx;
+        static_cast<S *>(cx.msplit)[(slab * MMA_COLS + m) * cx.nrhs + r] = val;
+      } else {
+        const int q = red_iota ? row : cx.idx[B.red_off + row];
+        static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = val;
+      }
+    }
+  }
+  if (ADJ && tl.start == 0 && sidx == 0 && B.n_skel > 0) {
+    for (int e = threadIdx.x; e < B.n_skel * NRT; e += MM_THREADS) {
+      const int i = e % B.n_skel, r = rhs0 + e / B.n_skel;
+      if (r >= cx.nrhs) continue;
+      const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
+      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = adj_in<S>(cx, B, i, r, from_f != 0);
+    }
+  }
+  if (ADJ && ksplit) {
+    // the last split of (block, column tile, RHS chunk) to arrive sums the
+    // slabs in split order (deterministic) and writes the partials
+    int &last = *flag;  // operand buffers are free after the K loop
+    __threadfence();
+    consumer_sync<BAR>();
+    const int grp = tl.pad >> 8;
+    int *cnt = cx.mcount + (int64_t)grp * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0) last = atomicAdd(cnt, 1) == B.mks - 1;
+    consumer_sync<BAR>();
+    if (!last) return;
+    __threadfence();
+    const int64_t slab0 = B.msp_off + (int64_t)(tl.start / MMA_COLS) * B.mks;
+    const S *scr = static_cast<const S *>(cx.msplit);
+    for (int e = threadIdx.x; e < tl.count * NRT; e += MM_THREADS) {
+      const int m = e / NRT, r = rhs0 + e % NRT;
+      if (r >= cx.nrhs) continue;
+      S sum = X::zero();
+      for (int k = 0; k < B.mks; ++k) sum = X::add(sum, X::ldcg(scr + ((slab0 + k) * MMA_COLS + m) * cx.nrhs + r));
+      const int row = tl.start + m;
+      const int q = red_iota ? row : cx.idx[B.red_off + row];
+      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = sum;
+    }
+    if (threadIdx.x == 0) *cnt = 0;  // re-arm for the next apply
+  }
+}
+
 template <class S, bool ADJ, int NT, bool M3, int MINB>
 __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, const Tile *__restrict__ tiles, int from_f) {
   using X = Tr<S>;
@@ -611,74 +705,258 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
     cp_async_wait<0>();
     __syncthreads();
   }
-  // epilogue: C fragment (row gid / gid+8, cols 2 tig / 2 tig + 1)
+  mma_epilogue<S, ADJ, NT, M3, 0>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
+}
+
+// ------------------------------------------------------------------------
+// Warp-specialised multi-RHS kernel.  Same tile, operand fragment order, K
+// split and epilogue as mma_kernel, but the operand loads move to a fifth
+// PRODUCER warp: it streams the factor tile with cp.async (completion
+// tracked by an mbarrier, cp.async.mbarrier.arrive.noinc) and gathers the
+// right-hand-side rows through registers into shared memory, NS stages ahead.
+// The four CONSUMER warps only wait on the stage's "full" barrier, run the
+// LDS + DMMA k4 steps and release the stage on its "empty" barrier: no block-
+// wide barrier and no load code between their DMMAs.
+// ------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_cp_async_arrive(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int WS_STAGES = 3;
+constexpr int WS_THREADS = MM_THREADS + 32;
+
+template <class S, bool ADJ, bool M3>
+__host__ __device__ constexpr int ws_smem_bytes() {
+  // NS x (A chunk + B chunk) operand buffers + 2 NS mbarriers
+  return WS_STAGES * (mm_bk<S>() / 4 * (MM_BM / 16) * 2 * 32 + mm_bk<S>() / 4 * 4 * 32) * (int)sizeof(S) +
+         2 * WS_STAGES * 8;
+}
+
+template <class S, bool ADJ, bool M3, int MINB>
+__global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, const Tile *__restrict__ tiles,
+                                                                  int from_f) {
+  using X = Tr<S>;
+  using PL = Planes<S>;
+  constexpr int NT = 4;
+  constexpr bool CPLX = PL::cplx;
+  constexpr bool G3 = CPLX && M3;
+  constexpr int NRT = 8 * NT;
+  constexpr int BK = mm_bk<S>();
+  constexpr int KS = BK / 4;
+  constexpr int AW = MM_BM / 16;
+  constexpr int A_CH = KS * AW * 2 * 32;
+  constexpr int B_CH = KS * NT * 32;
+  constexpr int NS = WS_STAGES;
+  extern __shared__ __align__(16) unsigned char ws_smem[];
+  S *As = reinterpret_cast<S *>(ws_smem);
+  S *Bs = As + NS * A_CH;
+  uint64_t *full = reinterpret_cast<uint64_t *>(Bs + NS * B_CH);
+  uint64_t *empty = full + NS;
+
+  const Tile tl = tiles[blockIdx.y];
+  const DevBlock B = cx.blocks[tl.blk];
+  const int rhs0 = blockIdx.x * NRT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
+  const int64_t ld = B.ld;
+  const int K = ADJ ? B.r_out : B.n_red;
+  const bool ksplit = ADJ && tl.pad >= 0;
+  const int sidx = ksplit ? (tl.pad & 255) : 0;
+  int kbeg = 0, kend = K;
+  if (ksplit) {
+    const int chunk = ((K + B.mks - 1) / B.mks + BK - 1) / BK * BK;
+    kbeg = min(K, sidx * chunk);
+    kend = min(K, kbeg + chunk);
+  }
+  const int nchunks = (kend - kbeg + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(full + i, 64);   // producer: 32 cp.async arrivals + 32 plain arrivals
+      mbar_init(empty + i, AW);  // one arrival per consumer warp
+    }
+  }
+  __syncthreads();
+
+  if (warp == AW) {
+    // ------------------------------------------------ producer warp
+    // B slot e = lane + 32 i holds row k = 4 (i / NT) + (lane & 3), rhs
+    // rhs0 + 8 (i % NT) + (lane >> 2): a lane touches KS rows per chunk, whose
+    // gather indices (redundant positions / perm_x) are prefetched one chunk
+    // ahead; the values then go straight to shared memory by cp.async.
+    const bool red_iota = (B.flags & F_RED_IOTA) != 0;
+    const bool from_f_ = from_f != 0;
+    const bool reg_path = cx.diag != nullptr;  // a fused diagonal needs the value in registers
+    const int tig_ = lane & 3, gid_ = lane >> 2;
+    auto row_index = [&](int kc, int k4) -> int {  // what the gather needs for row k of chunk kc
+      const int k = kbeg + kc * BK + 4 * k4 + tig_;
+      if (k >= kend) return -1;
+      if (ADJ) return from_f_ ? __ldg(cx.perm + B.out_off + k) : k;
+      return red_iota ? k : __ldg(cx.idx + B.red_off + k);
+    };
+    int qn[KS];
 #pragma unroll
-  for (int t = 0; t < NT; ++t) {
+    for (int k4 = 0; k4 < KS; ++k4) qn[k4] = nchunks > 0 ? row_index(0, k4) : -1;
+    for (int kc = 0; kc < nchunks; ++kc) {
+      const int slot = kc % NS;
+      int q[KS];
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int m = warp * 16 + gid + 8 * (v >> 1);
-      const int r = rhs0 + t * 8 + 2 * tig + (v & 1);
-      if (m >= tl.count || r >= cx.nrhs) continue;
-      S val;
-      if constexpr (!CPLX) {
-        val = c0[t][v];
-      } else if constexpr (G3) {
-        val = make_double2(c0[t][v] - c1[t][v], c2[t][v] - c0[t][v] - c1[t][v]);
-      } else {
-        val = make_double2(c0[t][v], c1[t][v]);
+      for (int k4 = 0; k4 < KS; ++k4) q[k4] = qn[k4];
+      if (kc + 1 < nchunks) {
+#pragma unroll
+        for (int k4 = 0; k4 < KS; ++k4) qn[k4] = row_index(kc + 1, k4);
       }
-      const int row = tl.start + m;
-      if (!ADJ) {
-        if (row < B.n_skel) {
-          const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
-          val = X::add(val, in_value<S>(cx, B, q, r));
+      mbar_wait(empty + slot, ((kc / NS) & 1) ^ 1);
+      const int kb = kbeg + kc * BK;
+      S *dA = As + slot * A_CH;
+#pragma unroll 4
+      for (int i = 0; i < A_CH / 32; ++i) {
+        const int e = lane + 32 * i;
+        const int tg = e & 3, gd = (e >> 2) & 7, hi = (e >> 5) & 1, w = (e >> 6) & (AW - 1), k4 = e >> 8;
+        const int m = w * 16 + hi * 8 + gd, k = k4 * 4 + tg;
+        const bool ok = m < tl.count && kb + k < kend;
+        const S *src = ADJ ? T + (int64_t)(tl.start + m) * ld + (kb + k) : T + (int64_t)(kb + k) * ld + (tl.start + m);
+        cp_async<sizeof(S)>(dA + e, ok ? src : T, ok);
+      }
+      S *dB = Bs + slot * B_CH;
+#pragma unroll
+      for (int i = 0; i < B_CH / 32; ++i) {
+        const int k4 = i / NT, t = i % NT;
+        const int r = rhs0 + t * 8 + gid_;
+        const int qq = q[k4];
+        const bool ok = qq >= 0 && r < cx.nrhs;
+        const S *src = static_cast<const S *>(cx.z);  // any valid address when !ok (zero fill)
+        if (ok) {
+          if (ADJ) {
+            src = from_f_ ? static_cast<const S *>(cx.fin) + (int64_t)r * cx.n + qq
+                          : static_cast<const S *>(cx.z) + (B.out_off + qq) * cx.nrhs + r;
+          } else {
+            const bool s1 = qq >= B.seg_len[0];
+            const int64_t off = s1 ? B.seg_off[1] + (qq - B.seg_len[0]) : B.seg_off[0] + qq;
+            const int32_t srcsel = s1 ? B.seg_src[1] : B.seg_src[0];
+            src = srcsel == SRC_C ? static_cast<const S *>(cx.c) + (int64_t)r * cx.m + off
+                                  : static_cast<const S *>(cx.z) + off * cx.nrhs + r;
+          }
         }
-        if (B.flags & F_OUT_F)
-          static_cast<S *>(cx.fout)[r * cx.n + cx.perm[B.out_off + row]] = val;
-        else
-          static_cast<S *>(cx.z)[(B.out_off + row) * cx.nrhs + r] = val;
-      } else if (ksplit) {
-        const int64_t slab = B.msp_off + (int64_t)(tl.start / MMA_COLS) * B.mks + sidx;
-        static_cast<S *>(cx.msplit)[(slab * MMA_COLS + m) * cx.nrhs + r] = val;
-      } else {
-        const int q = red_iota ? row : cx.idx[B.red_off + row];
-        static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = val;
+        if (!reg_path) {
+          cp_async<sizeof(S)>(dB + lane + 32 * i, src, ok);
+        } else {
+          dB[lane + 32 * i] = ok ? (ADJ ? *src : in_value<S>(cx, B, qq, r)) : X::zero();
+        }
+      }
+      mbar_cp_async_arrive(full + slot);  // completes when this lane's cp.async have landed
+      mbar_arrive(full + slot);           // the register-path stores (if any) are done
+    }
+    return;  // the producer takes no part in the epilogue
+  }
+
+  // ------------------------------------------------ consumer warps
+  const int gid = lane >> 2, tig = lane & 3;
+  double c0[NT][4], c1[NT][4], c2[G3 ? NT : 1][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) c0[t][v] = c1[t][v] = 0.0;
+#pragma unroll
+  for (int t = 0; t < (G3 ? NT : 1); ++t)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) c2[t][v] = 0.0;
+  (void)gid;
+  (void)tig;
+  for (int kc = 0; kc < nchunks; ++kc) {
+    const int slot = kc % NS;
+    mbar_wait(full + slot, (kc / NS) & 1);
+    const S *Ac = As + slot * A_CH;
+    const S *Bc = Bs + slot * B_CH;
+#pragma unroll
+    for (int k4 = 0; k4 < KS; ++k4) {
+      const S a0 = Ac[((k4 * AW + warp) * 2 + 0) * 32 + lane];
+      const S a1 = Ac[((k4 * AW + warp) * 2 + 1) * 32 + lane];
+      const double ar0 = PL::re(a0), ar1 = PL::re(a1);
+      const double ai0 = ADJ ? -PL::im(a0) : PL::im(a0), ai1 = ADJ ? -PL::im(a1) : PL::im(a1);
+      const double as0 = ar0 + ai0, as1 = ar1 + ai1;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const S b = Bc[(k4 * NT + t) * 32 + lane];
+        if constexpr (!CPLX) {
+          dmma(c0[t], ar0, ar1, PL::re(b));
+        } else if constexpr (G3) {
+          dmma(c0[t], ar0, ar1, PL::re(b));
+          dmma(c1[t], ai0, ai1, PL::im(b));
+          dmma(c2[t], as0, as1, PL::re(b) + PL::im(b));
+        } else {
+          dmma(c0[t], ar0, ar1, PL::re(b));
+          dmma(c0[t], -ai0, -ai1, PL::im(b));
+          dmma(c1[t], ar0, ar1, PL::im(b));
+          dmma(c1[t], ai0, ai1, PL::re(b));
+        }
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + slot);
   }
-  if (ADJ && tl.start == 0 && sidx == 0 && B.n_skel > 0) {
-    for (int e = threadIdx.x; e < B.n_skel * NRT; e += MM_THREADS) {
-      const int i = e % B.n_skel, r = rhs0 + e / B.n_skel;
-      if (r >= cx.nrhs) continue;
-      const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
-      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = adj_in<S>(cx, B, i, r, from_f != 0);
-    }
-  }
-  if (ADJ && ksplit) {
-    // the last split of (block, column tile, RHS chunk) to arrive sums the
-    // slabs in split order (deterministic) and writes the partials
-    int &last = *reinterpret_cast<int *>(As);  // operand buffers are free after the K loop
-    __threadfence();
-    __syncthreads();
-    const int grp = tl.pad >> 8;
-    int *cnt = cx.mcount + (int64_t)grp * gridDim.x + blockIdx.x;
-    if (threadIdx.x == 0) last = atomicAdd(cnt, 1) == B.mks - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    const int64_t slab0 = B.msp_off + (int64_t)(tl.start / MMA_COLS) * B.mks;
-    const S *scr = static_cast<const S *>(cx.msplit);
-    for (int e = threadIdx.x; e < tl.count * NRT; e += MM_THREADS) {
-      const int m = e / NRT, r = rhs0 + e % NRT;
-      if (r >= cx.nrhs) continue;
-      S sum = X::zero();
-      for (int k = 0; k < B.mks; ++k) sum = X::add(sum, X::ldcg(scr + ((slab0 + k) * MMA_COLS + m) * cx.nrhs + r));
-      const int row = tl.start + m;
-      const int q = red_iota ? row : cx.idx[B.red_off + row];
-      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = sum;
-    }
-    if (threadIdx.x == 0) *cnt = 0;  // re-arm for the next apply
-  }
+  // all consumer warps are past their last read of the operand buffers
+  consumer_sync<1>();
+  mma_epilogue<S, ADJ, NT, M3, 1>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
+}
+
+// warp-specialised kernels: opt-in (MHT_MMA_WS=1).  Measured slower than the
+// classic kernel: one producer warp cannot issue the cp.async / gather stream
+// fast enough (profiles/r01_mma_ws_ab.txt)
+inline bool mma_ws() {
+  static bool v = [] {
+    const char *e = getenv("MHT_MMA_WS");
+    return e && atoi(e) == 1;
+  }();
+  return v;
+}
+
+// CTAs per SM the warp-specialised kernel's registers are sized for: 3
+// (<= 136 registers) by default, MHT_MMA_WS_MINB=2 for the unconstrained build
+inline int mma_ws_minb() {
+  static int v = [] {
+    const char *e = getenv("MHT_MMA_WS_MINB");
+    return (e && atoi(e) == 2) ? 2 : 3;
+  }();
+  return v;
+}
+
+template <class S, bool ADJ, bool M3, int MINB>
+void mma_ws_launch_t(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
+  constexpr int smem = ws_smem_bytes<S, ADJ, M3>();
+  static bool attr = [] {
+    cudaFuncSetAttribute(mma_ws_kernel<S, ADJ, M3, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return true;
+  }();
+  (void)attr;
+  mma_ws_kernel<S, ADJ, M3, MINB><<<dim3((cx.nrhs + 31) / 32, nt), WS_THREADS, smem, st>>>(cx, tiles, from_f);
+}
+
+template <class S, bool ADJ, bool M3>
+void mma_ws_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
+  if (mma_ws_minb() == 2)
+    mma_ws_launch_t<S, ADJ, M3, 2>(cx, tiles, nt, from_f, st);
+  else
+    mma_ws_launch_t<S, ADJ, M3, 3>(cx, tiles, nt, from_f, st);
 }
 
 // Multi-RHS configuration (compile-time variants; default picked from the
@@ -713,7 +991,12 @@ void mma_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cuda
   for (int t0 = 0; t0 < ntiles; t0 += 65535) {
     const int nt = ntiles - t0 < 65535 ? ntiles - t0 : 65535;
     const int v = Planes<S>::cplx ? mma_variant() : 0;
-    if (v >= 1)
+    if (cx.nrhs >= 32 && mma_ws()) {
+      if (v >= 1)
+        mma_ws_launch<S, ADJ, true>(cx, tiles + t0, nt, from_f, st);
+      else
+        mma_ws_launch<S, ADJ, false>(cx, tiles + t0, nt, from_f, st);
+    } else if (v >= 1)
       mma_launch_nt<S, ADJ, true, 3, 4>(cx, tiles + t0, nt, from_f, st);
     else
       mma_launch_nt<S, ADJ, false, 4, 4>(cx, tiles + t0, nt, from_f, st);
