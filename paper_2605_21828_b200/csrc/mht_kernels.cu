@@ -741,14 +741,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// TMA 1-D bulk copy global -> shared, completion counted in bytes on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void *smem, const void *gmem, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
 constexpr int WS_STAGES = 3;
 constexpr int WS_THREADS = MM_THREADS + 32;
+// padded leading dimensions of the factor tile in shared memory (elements):
+// forward column-major [k][m] with AP = 64 + (2 complex | 4 real), adjoint
+// row-major [m][k] with BKP = BK + 4; chosen so a warp's A-fragment loads hit
+// distinct banks (16-byte slots 2 tig + gid / 4 gid + tig distinct mod 8 per
+// quarter warp; 8-byte slots distinct mod 16 per half warp)
+template <class S, bool ADJ>
+__host__ __device__ constexpr int ws_a_elems() {
+  return ADJ ? MM_BM * (mm_bk<S>() + 4) : mm_bk<S>() * (MM_BM + (sizeof(S) == 16 ? 2 : 4));
+}
 
 template <class S, bool ADJ, bool M3>
 __host__ __device__ constexpr int ws_smem_bytes() {
-  // NS x (A chunk + B chunk) operand buffers + 2 NS mbarriers
-  return WS_STAGES * (mm_bk<S>() / 4 * (MM_BM / 16) * 2 * 32 + mm_bk<S>() / 4 * 4 * 32) * (int)sizeof(S) +
-         2 * WS_STAGES * 8;
+  // NS x (A tile + B chunk) operand buffers + 2 NS mbarriers
+  return WS_STAGES * (ws_a_elems<S, ADJ>() + mm_bk<S>() / 4 * 4 * 32) * (int)sizeof(S) + 2 * WS_STAGES * 8;
 }
 
 template <class S, bool ADJ, bool M3, int MINB>
@@ -763,10 +785,11 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   constexpr int BK = mm_bk<S>();
   constexpr int KS = BK / 4;
   constexpr int AW = MM_BM / 16;
-  constexpr int A_CH = KS * AW * 2 * 32;
+  constexpr int A_CH = ws_a_elems<S, ADJ>();
+  constexpr int AP = ADJ ? BK + 4 : MM_BM + (sizeof(S) == 16 ? 2 : 4);  // padded leading dimension
   constexpr int B_CH = KS * NT * 32;
   constexpr int NS = WS_STAGES;
-  extern __shared__ __align__(16) unsigned char ws_smem[];
+  extern __shared__ __align__(128) unsigned char ws_smem[];
   S *As = reinterpret_cast<S *>(ws_smem);
   S *Bs = As + NS * A_CH;
   uint64_t *full = reinterpret_cast<uint64_t *>(Bs + NS * B_CH);
@@ -791,7 +814,7 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
-      mbar_init(full + i, 64);   // producer: 32 cp.async arrivals + 32 plain arrivals
+      mbar_init(full + i, 65);   // producer: 1 expect-tx arrival (TMA bytes) + 32 cp.async + 32 plain
       mbar_init(empty + i, AW);  // one arrival per consumer warp
     }
   }
@@ -827,15 +850,31 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
       }
       mbar_wait(empty + slot, ((kc / NS) & 1) ^ 1);
       const int kb = kbeg + kc * BK;
+      const int kn = min(BK, kend - kb);  // valid k of this chunk
       S *dA = As + slot * A_CH;
-#pragma unroll 4
-      for (int i = 0; i < A_CH / 32; ++i) {
-        const int e = lane + 32 * i;
-        const int tg = e & 3, gd = (e >> 2) & 7, hi = (e >> 5) & 1, w = (e >> 6) & (AW - 1), k4 = e >> 8;
-        const int m = w * 16 + hi * 8 + gd, k = k4 * 4 + tg;
-        const bool ok = m < tl.count && kb + k < kend;
-        const S *src = ADJ ? T + (int64_t)(tl.start + m) * ld + (kb + k) : T + (int64_t)(kb + k) * ld + (tl.start + m);
-        cp_async<sizeof(S)>(dA + e, ok ? src : T, ok);
+      // factor tile by TMA bulk copies (16-byte multiples: the real layout has
+      // even ld and a zero pad row, so an odd length rounds up into it)
+      constexpr int EV = sizeof(S) == 8 ? 2 : 1;
+      if (!ADJ) {
+        // forward: column k of the tile = tl.count contiguous rows of T
+        const unsigned cb = (unsigned)((tl.count + EV - 1) / EV * EV * sizeof(S));
+        if (lane == 0) mbar_arrive_expect_tx(full + slot, cb * kn);
+        for (int j = lane; j < BK; j += 32) {
+          if (j < kn) {
+            bulk_g2s(dA + j * AP, T + (int64_t)(kb + j) * ld + tl.start, cb, full + slot);
+          } else {  // K tail: zero column (stale shared memory could hold NaN patterns)
+            for (int i = 0; i < MM_BM; ++i) dA[j * AP + i] = X::zero();
+          }
+        }
+      } else {
+        // adjoint: row m of the tile = kn contiguous entries of T's column tl.start + m
+        const unsigned rb = (unsigned)((kn + EV - 1) / EV * EV * sizeof(S));
+        if (lane == 0) mbar_arrive_expect_tx(full + slot, rb * (unsigned)tl.count);
+        for (int m = lane; m < MM_BM; m += 32) {
+          if (m < tl.count) bulk_g2s(dA + m * AP, T + (int64_t)(tl.start + m) * ld + kb, rb, full + slot);
+          if (kn < BK)  // K tail: zero the rest of the row
+            for (int k = (kn + EV - 1) / EV * EV; k < BK; ++k) dA[m * AP + k] = X::zero();
+        }
       }
       S *dB = Bs + slot * B_CH;
 #pragma unroll
@@ -880,17 +919,17 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   for (int t = 0; t < (G3 ? NT : 1); ++t)
 #pragma unroll
     for (int v = 0; v < 4; ++v) c2[t][v] = 0.0;
-  (void)gid;
-  (void)tig;
   for (int kc = 0; kc < nchunks; ++kc) {
     const int slot = kc % NS;
     mbar_wait(full + slot, (kc / NS) & 1);
     const S *Ac = As + slot * A_CH;
     const S *Bc = Bs + slot * B_CH;
+    const int m0 = warp * 16 + gid;
 #pragma unroll
     for (int k4 = 0; k4 < KS; ++k4) {
-      const S a0 = Ac[((k4 * AW + warp) * 2 + 0) * 32 + lane];
-      const S a1 = Ac[((k4 * AW + warp) * 2 + 1) * 32 + lane];
+      const int k = 4 * k4 + tig;
+      const S a0 = ADJ ? Ac[m0 * AP + k] : Ac[k * AP + m0];
+      const S a1 = ADJ ? Ac[(m0 + 8) * AP + k] : Ac[k * AP + m0 + 8];
       const double ar0 = PL::re(a0), ar1 = PL::re(a1);
       const double ai0 = ADJ ? -PL::im(a0) : PL::im(a0), ai1 = ADJ ? -PL::im(a1) : PL::im(a1);
       const double as0 = ar0 + ai0, as1 = ar1 + ai1;
@@ -919,15 +958,25 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   mma_epilogue<S, ADJ, NT, M3, 1>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
 }
 
-// warp-specialised kernels: opt-in (MHT_MMA_WS=1).  Measured slower than the
-// classic kernel: one producer warp cannot issue the cp.async / gather stream
-// fast enough (profiles/r01_mma_ws_ab.txt)
-inline bool mma_ws() {
-  static bool v = [] {
+// Which multi-RHS launches use the warp-specialised TMA kernel
+// (profiles/r01_mma_ws_ab.txt): complex forward by default (c2: 18.1 vs
+// 21.5 ms, 0.94 of the DMMA peak); the adjoint (64 small row copies per
+// chunk, 2 CTAs/SM by shared memory) and real plans (32 gathers per producer
+// lane) stay on the classic kernel.  MHT_MMA_WS=0 never, =1 always.
+inline int mma_ws_mode() {
+  static int v = [] {
     const char *e = getenv("MHT_MMA_WS");
-    return e && atoi(e) == 1;
+    if (e && atoi(e) == 0) return 0;
+    if (e && atoi(e) == 1) return 1;
+    return -1;
   }();
   return v;
+}
+template <class S, bool ADJ>
+inline bool mma_ws() {
+  const int mode = mma_ws_mode();
+  if (mode >= 0) return mode == 1;
+  return Planes<S>::cplx && !ADJ;
 }
 
 // CTAs per SM the warp-specialised kernel's registers are sized for: 3
@@ -991,7 +1040,7 @@ void mma_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cuda
   for (int t0 = 0; t0 < ntiles; t0 += 65535) {
     const int nt = ntiles - t0 < 65535 ? ntiles - t0 : 65535;
     const int v = Planes<S>::cplx ? mma_variant() : 0;
-    if (cx.nrhs >= 32 && mma_ws()) {
+    if (cx.nrhs >= 32 && mma_ws<S, ADJ>()) {
       if (v >= 1)
         mma_ws_launch<S, ADJ, true>(cx, tiles + t0, nt, from_f, st);
       else
