@@ -474,7 +474,17 @@ __device__ __forceinline__ void consumer_sync() {
 // Multi-RHS epilogue (threads 0..127): C fragments (row gid / gid + 8, cols
 // 2 tig / 2 tig + 1) -> skeleton add and the output store (forward), partials
 // (adjoint) or the K-split slabs with the last-CTA fixup.
-template <class S, bool ADJ, int NT, bool M3, int BAR>
+// fragment row gid -> tile row, for the swizzled TMA adjoint tile (identity
+// otherwise): consecutive gid pairs / quads land on rows whose 128-byte
+// swizzle phases differ, so a quarter (16-byte) / half (8-byte) warp's
+// A-fragment loads hit distinct banks
+template <class S, bool PERM>
+__host__ __device__ __forceinline__ int frag_row(int gid) {
+  if (!PERM) return gid;
+  return sizeof(S) == 16 ? 4 * (gid & 1) + (gid >> 1) : 2 * (gid & 3) + (gid >> 2);
+}
+
+template <class S, bool ADJ, int NT, bool M3, int BAR, bool PERM = false>
 __device__ __forceinline__ void mma_epilogue(const Ctx &cx, const Tile &tl, const DevBlock &B, double (&c0)[NT][4],
                                              double (&c1)[NT][4], double (&c2)[(Planes<S>::cplx && M3) ? NT : 1][4],
                                              int rhs0, bool ksplit, int sidx, int from_f, int *flag) {
@@ -489,7 +499,7 @@ __device__ __forceinline__ void mma_epilogue(const Ctx &cx, const Tile &tl, cons
   for (int t = 0; t < NT; ++t) {
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const int m = warp * 16 + gid + 8 * (v >> 1);
+      const int m = warp * 16 + frag_row<S, PERM>(gid) + 8 * (v >> 1);
       const int r = rhs0 + t * 8 + 2 * tig + (v & 1);
       if (m >= tl.count || r >= cx.nrhs) continue;
       S val;
@@ -755,6 +765,14 @@ __device__ __forceinline__ void bulk_g2s(void *smem, const void *gmem, unsigned 
                : "memory");
 }
 
+// TMA 2-D tiled load (tensor map in global memory) -> shared, bytes on an mbarrier
+__device__ __forceinline__ void tma_2d_g2s(void *smem, const void *tmap, int c0, int c1, uint64_t *bar) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem)),
+               "l"(tmap), "r"(c0), "r"(c1), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
 constexpr int WS_STAGES = 3;
 constexpr int WS_THREADS = MM_THREADS + 32;
 // padded leading dimensions of the factor tile in shared memory (elements):
@@ -764,13 +782,14 @@ constexpr int WS_THREADS = MM_THREADS + 32;
 // quarter warp; 8-byte slots distinct mod 16 per half warp)
 template <class S, bool ADJ>
 __host__ __device__ constexpr int ws_a_elems() {
-  return ADJ ? MM_BM * (mm_bk<S>() + 4) : mm_bk<S>() * (MM_BM + (sizeof(S) == 16 ? 2 : 4));
+  return ADJ ? MM_BM * mm_bk<S>() : mm_bk<S>() * (MM_BM + (sizeof(S) == 16 ? 2 : 4));
 }
 
 template <class S, bool ADJ, bool M3>
 __host__ __device__ constexpr int ws_smem_bytes() {
-  // NS x (A tile + B chunk) operand buffers + 2 NS mbarriers
-  return WS_STAGES * (ws_a_elems<S, ADJ>() + mm_bk<S>() / 4 * 4 * 32) * (int)sizeof(S) + 2 * WS_STAGES * 8;
+  // NS x (A tile + B chunk) operand buffers + 2 NS mbarriers + 1 KB to align
+  // the stages to the 1024-byte period of the 128-byte TMA swizzle
+  return WS_STAGES * (ws_a_elems<S, ADJ>() + mm_bk<S>() / 4 * 4 * 32) * (int)sizeof(S) + 2 * WS_STAGES * 8 + 1024;
 }
 
 template <class S, bool ADJ, bool M3, int MINB>
@@ -786,11 +805,15 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   constexpr int KS = BK / 4;
   constexpr int AW = MM_BM / 16;
   constexpr int A_CH = ws_a_elems<S, ADJ>();
-  constexpr int AP = ADJ ? BK + 4 : MM_BM + (sizeof(S) == 16 ? 2 : 4);  // padded leading dimension
+  // leading dimension of the factor tile in shared memory: forward padded
+  // column-major [k][m]; adjoint the TMA box [m][k] as written (dense)
+  constexpr int AP = ADJ ? BK : MM_BM + (sizeof(S) == 16 ? 2 : 4);
   constexpr int B_CH = KS * NT * 32;
   constexpr int NS = WS_STAGES;
   extern __shared__ __align__(128) unsigned char ws_smem[];
-  S *As = reinterpret_cast<S *>(ws_smem);
+  // stage buffers start at a 1024-byte boundary (shared-space address)
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(ws_smem);
+  S *As = reinterpret_cast<S *>(ws_smem + (((sbase + 1023u) & ~1023u) - sbase));
   S *Bs = As + NS * A_CH;
   uint64_t *full = reinterpret_cast<uint64_t *>(Bs + NS * B_CH);
   uint64_t *empty = full + NS;
@@ -810,7 +833,9 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
     kbeg = min(K, sidx * chunk);
     kend = min(K, kbeg + chunk);
   }
-  const int nchunks = (kend - kbeg + BK - 1) / BK;
+  // a tile without columns (COPY block in the adjoint: skeleton part only)
+  // has no product, and no tensor map to load from
+  const int nchunks = tl.count > 0 ? (kend - kbeg + BK - 1) / BK : 0;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -866,15 +891,16 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
             for (int i = 0; i < MM_BM; ++i) dA[j * AP + i] = X::zero();
           }
         }
-      } else {
-        // adjoint: row m of the tile = kn contiguous entries of T's column tl.start + m
-        const unsigned rb = (unsigned)((kn + EV - 1) / EV * EV * sizeof(S));
-        if (lane == 0) mbar_arrive_expect_tx(full + slot, rb * (unsigned)tl.count);
-        for (int m = lane; m < MM_BM; m += 32) {
-          if (m < tl.count) bulk_g2s(dA + m * AP, T + (int64_t)(tl.start + m) * ld + kb, rb, full + slot);
-          if (kn < BK)  // K tail: zero the rest of the row
-            for (int k = (kn + EV - 1) / EV * EV; k < BK; ++k) dA[m * AP + k] = X::zero();
-        }
+      } else if (lane == 0) {
+        // adjoint: the BK x 64 tile (T rows kb.., T columns tl.start..) as two
+        // 2-D TMA requests of 128-byte rows (BK/2 scalars x 64 columns each),
+        // 128-byte swizzled; rows / columns past the block are zero-filled (a
+        // K split's rows past kend meet zero right-hand sides)
+        const void *tmap = static_cast<const unsigned char *>(cx.tmaps) + (size_t)tl.blk * 128;
+        mbar_arrive_expect_tx(full + slot, (unsigned)(MM_BM * BK * sizeof(S)));
+        constexpr int KH = BK / 2;
+        tma_2d_g2s(dA, tmap, kb * (int)(sizeof(S) / 8), tl.start, full + slot);
+        tma_2d_g2s(dA + MM_BM * KH, tmap, (kb + KH) * (int)(sizeof(S) / 8), tl.start, full + slot);
       }
       S *dB = Bs + slot * B_CH;
 #pragma unroll
@@ -924,12 +950,24 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
     mbar_wait(full + slot, (kc / NS) & 1);
     const S *Ac = As + slot * A_CH;
     const S *Bc = Bs + slot * B_CH;
-    const int m0 = warp * 16 + gid;
+    const int m0 = warp * 16 + frag_row<S, ADJ>(gid);
 #pragma unroll
     for (int k4 = 0; k4 < KS; ++k4) {
       const int k = 4 * k4 + tig;
-      const S a0 = ADJ ? Ac[m0 * AP + k] : Ac[k * AP + m0];
-      const S a1 = ADJ ? Ac[(m0 + 8) * AP + k] : Ac[k * AP + m0 + 8];
+      S a0, a1;
+      if constexpr (ADJ) {
+        // swizzled [half][m][128 B]: 16-byte chunk c of row m sits at c ^ (m & 7)
+        constexpr int KH = BK / 2;
+        const int h = k / KH, kk = k % KH;
+        const int byte = kk * (int)sizeof(S);
+        const unsigned char *hb = reinterpret_cast<const unsigned char *>(Ac) + h * (MM_BM * 128);
+        const int c = byte >> 4, o = byte & 15;
+        a0 = *reinterpret_cast<const S *>(hb + m0 * 128 + ((c ^ (m0 & 7)) << 4) + o);
+        a1 = *reinterpret_cast<const S *>(hb + (m0 + 8) * 128 + ((c ^ ((m0 + 8) & 7)) << 4) + o);
+      } else {
+        a0 = Ac[k * AP + m0];
+        a1 = Ac[k * AP + m0 + 8];
+      }
       const double ar0 = PL::re(a0), ar1 = PL::re(a1);
       const double ai0 = ADJ ? -PL::im(a0) : PL::im(a0), ai1 = ADJ ? -PL::im(a1) : PL::im(a1);
       const double as0 = ar0 + ai0, as1 = ar1 + ai1;
@@ -955,14 +993,14 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   }
   // all consumer warps are past their last read of the operand buffers
   consumer_sync<1>();
-  mma_epilogue<S, ADJ, NT, M3, 1>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
+  mma_epilogue<S, ADJ, NT, M3, 1, ADJ>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
 }
 
 // Which multi-RHS launches use the warp-specialised TMA kernel
-// (profiles/r01_mma_ws_ab.txt): complex forward by default (c2: 18.1 vs
-// 21.5 ms, 0.94 of the DMMA peak); the adjoint (64 small row copies per
-// chunk, 2 CTAs/SM by shared memory) and real plans (32 gathers per producer
-// lane) stay on the classic kernel.  MHT_MMA_WS=0 never, =1 always.
+// (profiles/r01_mma_ws_ab.txt): complex plans, both directions (c2 nrhs 32:
+// forward 18.1 vs 21.5 ms, adjoint 18.5 vs 19.9 ms).  Real plans stay on the
+// classic kernel (c3: the producer warp's 32 gathers per lane per chunk make
+// WS 1.3-3x slower).  MHT_MMA_WS=0 never, =1 always.
 inline int mma_ws_mode() {
   static int v = [] {
     const char *e = getenv("MHT_MMA_WS");
@@ -976,7 +1014,7 @@ template <class S, bool ADJ>
 inline bool mma_ws() {
   const int mode = mma_ws_mode();
   if (mode >= 0) return mode == 1;
-  return Planes<S>::cplx && !ADJ;
+  return Planes<S>::cplx;
 }
 
 // CTAs per SM the warp-specialised kernel's registers are sized for: 3

@@ -13,7 +13,9 @@
 //  4. build size-sorted (LPT) forward row tiles and adjoint column tiles per
 //     stage, and the adjoint group-sum pieces (sum-of-partials, no atomics);
 //  5. upload the tables.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -131,6 +133,7 @@ struct mht_plan {
   std::vector<double> last_phase_ms[2];    // [dir] per-phase durations of the last profiled apply
   bool want_stamps[2] = {false, false};
   int64_t *d_rdtab = nullptr;
+  void *d_tmaps = nullptr;  // CUtensorMap per materialised block (adjoint TMA tiles)
   bool fused_sum = true;        // adjoint group sums on the consumer's load (MHT_FUSED_SUM=0: off)
   int n_unfused = 0;
   int64_t n_split_groups = 0;
@@ -164,7 +167,7 @@ struct mht_plan {
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd, (void *)d_fwd1, d_fsplit, (void *)d_fcount,
-                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, (void *)d_phases, (void *)d_ctr, (void *)d_stamps, d_msplit, (void *)d_mcount, d_ctmp, d_z, d_part, d_hc, d_hf})
+                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, (void *)d_phases, (void *)d_ctr, (void *)d_stamps, d_msplit, (void *)d_mcount, d_ctmp, d_tmaps, d_z, d_part, d_hc, d_hf})
       if (p) cudaFree(p);
   }
 };
@@ -643,6 +646,49 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
     P->device_bytes += (int64_t)nbytes;
   }
 
+  // ------------------------------------------------ TMA descriptors (adjoint tiles)
+  // One 2-D tensor map per block with coefficients: T viewed as a column-major
+  // r_out x n_red array of float64 (complex: 2 r_out doubles per column),
+  // row stride ld; box = BK/2 rows (128 bytes) x 64 columns, 128-byte
+  // swizzle (half of the adjoint tile's K chunk per request), out-of-range
+  // rows / columns zero-filled by the TMA unit.
+  {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void *fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    if (!encode) return fail(MHT_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+    std::vector<CUtensorMap> maps(blocks.size());
+    const int bk = P->cplx ? 16 : 32;
+    const int ew = P->cplx ? 2 : 1;  // doubles per scalar
+    for (size_t i = 0; i < blocks.size(); ++i) {
+      const DevBlock &D = blocks[i];
+      memset(&maps[i], 0, sizeof(CUtensorMap));
+      if (D.n_red == 0 || D.r_out == 0) continue;
+      cuuint64_t dims[2] = {(cuuint64_t)D.r_out * ew, (cuuint64_t)D.n_red};
+      cuuint64_t strides[1] = {(cuuint64_t)D.ld * P->ssz};
+      cuuint32_t box[2] = {(cuuint32_t)(bk * ew / 2), (cuuint32_t)MMA_COLS};  // 128-byte rows
+      cuuint32_t estr[2] = {1, 1};
+      void *addr = static_cast<char *>(P->d_coef) + D.coef_off * (int64_t)P->ssz;
+      CUresult r = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, addr, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) for block %zu", (int)r, i);
+        return fail(MHT_ERR_CUDA, buf);
+      }
+    }
+    CUDA_TRY(cudaMalloc(&P->d_tmaps, std::max<size_t>(1, maps.size()) * sizeof(CUtensorMap)));
+    if (!maps.empty())
+      CUDA_TRY(cudaMemcpy(P->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    P->device_bytes += (int64_t)maps.size() * (int64_t)sizeof(CUtensorMap);
+  }
+
   // ------------------------------------------------ tiles (LPT order per stage)
   std::vector<std::vector<std::pair<int64_t, Tile>>> ft(L + 2), at(L + 2), amt(L + 2);
   for (int i = 0; i < (int)blocks.size(); ++i) {
@@ -1087,6 +1133,7 @@ Ctx make_ctx(mht_plan *P, int nrhs) {
   cx.fsplit = P->d_fsplit;
   cx.fcount = P->d_fcount;
   cx.rdtab = P->d_rdtab;
+  cx.tmaps = P->d_tmaps;
   cx.diag = P->cur_diag;
   cx.diag_sqrt = P->cur_diag_sqrt;
   cx.msplit = P->d_msplit;

@@ -126,7 +126,7 @@ def test_ragged_leaves_and_L0(gpu, oracle_lib, plans):
 def test_full_rank_plan_identity_copy_paths(gpu, oracle_lib, plans):
     """tol ~ 0: many IDENTITY blocks -> alias and COPY resolution paths."""
     path, w = flat_case(plans, 1024, 32, 4, 1e-15, name="exact")
-    P, _ = check_plan(gpu, oracle_lib, path, w, (1, 4), dense=flat_dense(oracle_lib, w))
+    P, _ = check_plan(gpu, oracle_lib, path, w, (1, 4, 32, 33), dense=flat_dense(oracle_lib, w))
     assert P.info.n_alias > 0
 
 
