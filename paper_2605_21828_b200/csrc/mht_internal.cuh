@@ -93,6 +93,7 @@ struct Ctx {  // per-launch pointers
   int diag_sqrt;         // g(d) = sqrt(d) (GRF sampling) instead of d
   const int64_t *rdtab;  // fused adjoint sums: reader partial offsets
   const void *tmaps;     // per-block 2-D TMA descriptors of T (CUtensorMap, 128 B each; adjoint tiles)
+  const void *tmaps_f;   // ... for the real forward tiles (16 rows x BK columns boxes)
   int fused;             // 1: adjoint inputs are summed from the partials on load
   int64_t m, n, Zt, Pt;  // Zt/Pt: workspace entries per RHS (layout [entry][rhs])
   int nrhs;

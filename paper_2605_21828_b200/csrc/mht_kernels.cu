@@ -484,7 +484,18 @@ __host__ __device__ __forceinline__ int frag_row(int gid) {
   return sizeof(S) == 16 ? 4 * (gid & 1) + (gid >> 1) : 2 * (gid & 3) + (gid >> 2);
 }
 
-template <class S, bool ADJ, int NT, bool M3, int BAR, bool PERM = false>
+// MMA row r (0..15, a0 rows 0..7, a1 rows 8..15) -> tile row within the warp's
+// 16-row slab.  MODE 0: identity; 1: swizzled adjoint tile (frag_row, a1 = a0
+// + 8); 2: swizzled real forward tile [k][16 rows] (quad q of rows -> tile rows
+// {2q, 2q+1, 2q+8, 2q+9}: the half warp's 8-byte loads hit 16 distinct banks)
+template <class S, int MODE>
+__host__ __device__ __forceinline__ int tile_row(int r) {
+  if (MODE == 0) return r;
+  if (MODE == 1) return frag_row<S, true>(r & 7) + 8 * (r >> 3);
+  return 2 * (r >> 2) + (r & 1) + 8 * ((r >> 1) & 1);
+}
+
+template <class S, bool ADJ, int NT, bool M3, int BAR, int MODE = 0>
 __device__ __forceinline__ void mma_epilogue(const Ctx &cx, const Tile &tl, const DevBlock &B, double (&c0)[NT][4],
                                              double (&c1)[NT][4], double (&c2)[(Planes<S>::cplx && M3) ? NT : 1][4],
                                              int rhs0, bool ksplit, int sidx, int from_f, int *flag) {
@@ -499,7 +510,7 @@ __device__ __forceinline__ void mma_epilogue(const Ctx &cx, const Tile &tl, cons
   for (int t = 0; t < NT; ++t) {
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const int m = warp * 16 + frag_row<S, PERM>(gid) + 8 * (v >> 1);
+      const int m = warp * 16 + tile_row<S, MODE>(gid + 8 * (v >> 1));
       const int r = rhs0 + t * 8 + 2 * tig + (v & 1);
       if (m >= tl.count || r >= cx.nrhs) continue;
       S val;
@@ -782,7 +793,14 @@ constexpr int WS_THREADS = MM_THREADS + 32;
 // quarter warp; 8-byte slots distinct mod 16 per half warp)
 template <class S, bool ADJ>
 __host__ __device__ constexpr int ws_a_elems() {
-  return ADJ ? MM_BM * mm_bk<S>() : mm_bk<S>() * (MM_BM + (sizeof(S) == 16 ? 2 : 4));
+  return (ADJ || sizeof(S) == 8) ? MM_BM * mm_bk<S>() : mm_bk<S>() * (MM_BM + 2);
+}
+// A-tile layout / row mapping of the warp-specialised kernel: 0 padded
+// column-major by 1-D bulk copies (complex forward), 1 swizzled [half][m][k]
+// by 2-D TMA (adjoint), 2 swizzled [quad][k][16 rows] by 2-D TMA (real forward)
+template <class S, bool ADJ>
+__host__ __device__ constexpr int ws_mode() {
+  return ADJ ? 1 : (sizeof(S) == 8 ? 2 : 0);
 }
 
 template <class S, bool ADJ, bool M3>
@@ -807,7 +825,8 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   constexpr int A_CH = ws_a_elems<S, ADJ>();
   // leading dimension of the factor tile in shared memory: forward padded
   // column-major [k][m]; adjoint the TMA box [m][k] as written (dense)
-  constexpr int AP = ADJ ? BK : MM_BM + (sizeof(S) == 16 ? 2 : 4);
+  constexpr int AP = ADJ ? BK : MM_BM + 2;  // (mode 0 only)
+  constexpr int MODE = ws_mode<S, ADJ>();
   constexpr int B_CH = KS * NT * 32;
   constexpr int NS = WS_STAGES;
   extern __shared__ __align__(128) unsigned char ws_smem[];
@@ -880,7 +899,16 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
       // factor tile by TMA bulk copies (16-byte multiples: the real layout has
       // even ld and a zero pad row, so an odd length rounds up into it)
       constexpr int EV = sizeof(S) == 8 ? 2 : 1;
-      if (!ADJ) {
+      if (MODE == 2) {
+        if (lane == 0) {
+          // real forward: the 64 x BK tile as four 2-D TMA requests of 16 rows
+          // (128 B) x BK columns, 128-byte swizzled, past-the-block zero-filled
+          const void *tmap = static_cast<const unsigned char *>(cx.tmaps_f) + (size_t)tl.blk * 128;
+          mbar_arrive_expect_tx(full + slot, (unsigned)(MM_BM * BK * sizeof(S)));
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) tma_2d_g2s(dA + q4 * BK * 16, tmap, tl.start + 16 * q4, kb, full + slot);
+        }
+      } else if (!ADJ) {
         // forward: column k of the tile = tl.count contiguous rows of T
         const unsigned cb = (unsigned)((tl.count + EV - 1) / EV * EV * sizeof(S));
         if (lane == 0) mbar_arrive_expect_tx(full + slot, cb * kn);
@@ -950,12 +978,18 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
     mbar_wait(full + slot, (kc / NS) & 1);
     const S *Ac = As + slot * A_CH;
     const S *Bc = Bs + slot * B_CH;
-    const int m0 = warp * 16 + frag_row<S, ADJ>(gid);
+    const int m0 = warp * 16 + tile_row<S, MODE>(gid), m1 = warp * 16 + tile_row<S, MODE>(gid + 8);
 #pragma unroll
     for (int k4 = 0; k4 < KS; ++k4) {
       const int k = 4 * k4 + tig;
       S a0, a1;
-      if constexpr (ADJ) {
+      if constexpr (MODE == 2) {
+        // swizzled [quad][k][16 rows]: 16-byte chunk c of row k sits at c ^ (k & 7)
+        const unsigned char *ab = reinterpret_cast<const unsigned char *>(Ac) + k * 128;
+        const int mm0 = m0 & 15, mm1 = m1 & 15;
+        a0 = *reinterpret_cast<const S *>(ab + (m0 >> 4) * (BK * 128) + (((mm0 >> 1) ^ (k & 7)) << 4) + (mm0 & 1) * 8);
+        a1 = *reinterpret_cast<const S *>(ab + (m1 >> 4) * (BK * 128) + (((mm1 >> 1) ^ (k & 7)) << 4) + (mm1 & 1) * 8);
+      } else if constexpr (ADJ) {
         // swizzled [half][m][128 B]: 16-byte chunk c of row m sits at c ^ (m & 7)
         constexpr int KH = BK / 2;
         const int h = k / KH, kk = k % KH;
@@ -963,10 +997,10 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
         const unsigned char *hb = reinterpret_cast<const unsigned char *>(Ac) + h * (MM_BM * 128);
         const int c = byte >> 4, o = byte & 15;
         a0 = *reinterpret_cast<const S *>(hb + m0 * 128 + ((c ^ (m0 & 7)) << 4) + o);
-        a1 = *reinterpret_cast<const S *>(hb + (m0 + 8) * 128 + ((c ^ ((m0 + 8) & 7)) << 4) + o);
+        a1 = *reinterpret_cast<const S *>(hb + m1 * 128 + ((c ^ (m1 & 7)) << 4) + o);
       } else {
         a0 = Ac[k * AP + m0];
-        a1 = Ac[k * AP + m0 + 8];
+        a1 = Ac[k * AP + m1];
       }
       const double ar0 = PL::re(a0), ar1 = PL::re(a1);
       const double ai0 = ADJ ? -PL::im(a0) : PL::im(a0), ai1 = ADJ ? -PL::im(a1) : PL::im(a1);
@@ -993,7 +1027,7 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   }
   // all consumer warps are past their last read of the operand buffers
   consumer_sync<1>();
-  mma_epilogue<S, ADJ, NT, M3, 1, ADJ>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
+  mma_epilogue<S, ADJ, NT, M3, 1, MODE>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
 }
 
 // Which multi-RHS launches use the warp-specialised TMA kernel

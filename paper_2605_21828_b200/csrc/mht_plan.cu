@@ -133,7 +133,8 @@ struct mht_plan {
   std::vector<double> last_phase_ms[2];    // [dir] per-phase durations of the last profiled apply
   bool want_stamps[2] = {false, false};
   int64_t *d_rdtab = nullptr;
-  void *d_tmaps = nullptr;  // CUtensorMap per materialised block (adjoint TMA tiles)
+  void *d_tmaps = nullptr;    // CUtensorMap per materialised block (adjoint TMA tiles)
+  void *d_tmaps_f = nullptr;  // ... real forward TMA tiles
   bool fused_sum = true;        // adjoint group sums on the consumer's load (MHT_FUSED_SUM=0: off)
   int n_unfused = 0;
   int64_t n_split_groups = 0;
@@ -167,7 +168,7 @@ struct mht_plan {
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd, (void *)d_fwd1, d_fsplit, (void *)d_fcount,
-                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, (void *)d_phases, (void *)d_ctr, (void *)d_stamps, d_msplit, (void *)d_mcount, d_ctmp, d_tmaps, d_z, d_part, d_hc, d_hf})
+                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, (void *)d_phases, (void *)d_ctr, (void *)d_stamps, d_msplit, (void *)d_mcount, d_ctmp, d_tmaps, d_tmaps_f, d_z, d_part, d_hc, d_hf})
       if (p) cudaFree(p);
   }
 };
@@ -687,6 +688,28 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
     if (!maps.empty())
       CUDA_TRY(cudaMemcpy(P->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     P->device_bytes += (int64_t)maps.size() * (int64_t)sizeof(CUtensorMap);
+    // real forward tiles: box = 16 rows (128 B) x BK columns, 128-byte swizzle
+    if (!P->cplx) {
+      std::vector<CUtensorMap> fmaps(blocks.size());
+      for (size_t i = 0; i < blocks.size(); ++i) {
+        const DevBlock &D = blocks[i];
+        memset(&fmaps[i], 0, sizeof(CUtensorMap));
+        if (D.n_red == 0 || D.r_out == 0) continue;
+        cuuint64_t dims[2] = {(cuuint64_t)D.r_out, (cuuint64_t)D.n_red};
+        cuuint64_t strides[1] = {(cuuint64_t)D.ld * P->ssz};
+        cuuint32_t box[2] = {16, (cuuint32_t)bk};
+        cuuint32_t estr[2] = {1, 1};
+        void *addr = static_cast<char *>(P->d_coef) + D.coef_off * (int64_t)P->ssz;
+        CUresult r = encode(&fmaps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, addr, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(MHT_ERR_CUDA, "cuTensorMapEncodeTiled failed (forward map)");
+      }
+      CUDA_TRY(cudaMalloc(&P->d_tmaps_f, std::max<size_t>(1, fmaps.size()) * sizeof(CUtensorMap)));
+      if (!fmaps.empty())
+        CUDA_TRY(cudaMemcpy(P->d_tmaps_f, fmaps.data(), fmaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+      P->device_bytes += (int64_t)fmaps.size() * (int64_t)sizeof(CUtensorMap);
+    }
   }
 
   // ------------------------------------------------ tiles (LPT order per stage)
@@ -1134,6 +1157,7 @@ Ctx make_ctx(mht_plan *P, int nrhs) {
   cx.fcount = P->d_fcount;
   cx.rdtab = P->d_rdtab;
   cx.tmaps = P->d_tmaps;
+  cx.tmaps_f = P->d_tmaps_f;
   cx.diag = P->cur_diag;
   cx.diag_sqrt = P->cur_diag_sqrt;
   cx.msplit = P->d_msplit;
