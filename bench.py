@@ -415,7 +415,9 @@ def main():
         achieved = alg / (per_launch_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["dmma_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["dmma_tflops"], "traffic": traffic, "algorithmic_flops_per_launch": alg,
-                "kernel": f"mma_kernel {dkind} nrhs={dr} (DMMA m16n8k4 f64)", "peak_source": peaks["dmma_src"]}
+                "kernel": (f"{'mma_ws_kernel' if P.is_complex else 'mma_kernel'} {dkind} nrhs={dr} "
+                           f"(DMMA m16n8k4 f64{', TMA + warp-specialised' if P.is_complex else ''})"),
+                "peak_source": peaks["dmma_src"]}
         if P.is_complex:
             roof["note"] = ("achieved counts 8 real flops per complex multiply-add (algorithmic); the kernel "
                             "issues 3 real DMMA products per complex product (Gauss), so pipe work is 3/4 of that")

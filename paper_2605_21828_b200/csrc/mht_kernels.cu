@@ -271,7 +271,7 @@ __device__ __forceinline__ S adj_in(const Ctx &cx, const DevBlock &B, int i, int
 // partial column sums to scratch and the last CTA of the group to arrive adds
 // them in split order (deterministic, no float atomics).
 // ------------------------------------------------------------------------
-template <class S, int RB, bool CG>
+template <class S, int RB, bool CG, int RCH = ADJ_RCH>
 __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_f, int rhs0) {
   using X = Tr<S>;
   // columns per warp: 8 complex / 16 real
@@ -288,7 +288,7 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
     rbeg = sidx * chunk;
     rend = min(B.r_out, rbeg + chunk);
   }
-  __shared__ S zs[ADJ_RCH][RB];
+  __shared__ S zs[RCH][RB];
   S acc[CPW][RB];
 #pragma unroll
   for (int u = 0; u < CPW; ++u)
@@ -300,8 +300,8 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
   const int cend = tl.start + tl.count;
   constexpr bool REAL = sizeof(S) == 8;
 
-  for (int rc = rbeg; rc < rend; rc += ADJ_RCH) {
-    const int rn = min(ADJ_RCH, rend - rc);
+  for (int rc = rbeg; rc < rend; rc += RCH) {
+    const int rn = min(RCH, rend - rc);
     for (int e = threadIdx.x; e < rn * RB; e += ADJ_THREADS) {
       const int i = e % rn, k = e / rn;
       zs[i][k] = (rhs0 + k < cx.nrhs) ? adj_in<S, CG>(cx, B, rc + i, rhs0 + k, from_f) : X::zero();
@@ -399,10 +399,19 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
   }
 }
 
-template <class S, int RB>
+template <class S, int RB, int RCH = ADJ_RCH>
 __global__ void __launch_bounds__(ADJ_THREADS, 7) adj_kernel(const Ctx cx, const Tile *__restrict__ tiles,
                                                              int from_f) {
-  adj_tile<S, RB, false>(cx, tiles[blockIdx.y], from_f, blockIdx.x * RB);
+  adj_tile<S, RB, false, RCH>(cx, tiles[blockIdx.y], from_f, blockIdx.x * RB);
+}
+
+// rows of z staged per pass: MHT_ADJ_RCH=512|1024 (experiments), default ADJ_RCH
+inline int adj_rch() {
+  static int v = [] {
+    const char *e = getenv("MHT_ADJ_RCH");
+    return e ? atoi(e) : ADJ_RCH;
+  }();
+  return v;
 }
 
 // ------------------------------------------------------------------------
@@ -1220,7 +1229,12 @@ template <class S>
 void adj_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
     const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
-    adj_kernel<S, 1><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+    if (adj_rch() == 1024)
+      adj_kernel<S, 1, 1024><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+    else if (adj_rch() == 512)
+      adj_kernel<S, 1, 512><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+    else
+      adj_kernel<S, 1><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
   }
 }
 

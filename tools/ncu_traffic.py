@@ -29,7 +29,7 @@ def phase_of(name: str, width: int) -> str | None:
         return "fwd@1"
     if name.startswith("adj_kernel"):
         return "adj@1"
-    if name.startswith("mma_kernel"):
+    if name.startswith("mma_kernel") or name.startswith("mma_ws_kernel"):
         args = name[name.index("<") + 1:].split(",")
         adj = args[1].strip() in ("1", "true")
         return f"{'adj' if adj else 'fwd'}@{width}"
