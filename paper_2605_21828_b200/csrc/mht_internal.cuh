@@ -91,6 +91,7 @@ struct Ctx {  // per-launch pointers
   const double *diag;    // optional real diagonal on the coefficient side (m entries):
                          // forward reads c_k * g(d_k), adjoint writes g(d_k) * c_k
   int diag_sqrt;         // g(d) = sqrt(d) (GRF sampling) instead of d
+  int b16;               // debug: 16-byte row gathers in the warp-specialised real kernel (MHT_WS_B16=0: off)
   const int64_t *rdtab;  // fused adjoint sums: reader partial offsets
   const void *tmaps;     // per-block 2-D TMA descriptors of T (CUtensorMap, 128 B each; adjoint tiles)
   const void *tmaps_f;   // ... for the real forward tiles (16 rows x BK columns boxes)
@@ -106,7 +107,8 @@ constexpr int ADJ_COLS_REAL = 64;  // ... real (16 per warp)
 template <class S>
 __host__ __device__ constexpr int adj_cols() { return sizeof(S) == 16 ? ADJ_COLS : ADJ_COLS_REAL; }
 constexpr int ADJ_THREADS = 128;
-constexpr int ADJ_RCH = 256;     // adjoint rows staged in smem per pass
+constexpr int ADJ_RCH = 1024;    // adjoint rows staged in smem per pass (most blocks: one pass;
+                                 // 256 / 512 measured 8% slower on c2, profiles/r01_adj_rch_ab.txt)
 constexpr int MMA_COLS = 64;     // redundant columns per multi-RHS adjoint tile
 
 // One phase of the persistent nrhs = 1 apply (a stage's tiles or a list of

@@ -126,7 +126,7 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
 // adds them in split order — deterministic, no float atomics.
 // ------------------------------------------------------------------------
 // CG: workspace reads through L2 only (the persistent kernel; see in_value)
-template <class S, bool CG>
+template <class S, bool CG, int FBT = 8>
 __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
   using X = Tr<S>;
   const DevBlock B = cx.blocks[tl.blk];
@@ -174,8 +174,31 @@ __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
       }
     };
     if (jn == 32) {
+      if constexpr (REAL && FBT == 0) {
+#pragma unroll 16
+        for (int jj = 0; jj < 32; ++jj) step(jj);
+      } else if constexpr (REAL) {
+        // each batch's FB loads issued before the first use (the interleaved
+        // form kept only ~4 loads outstanding per warp)
+        constexpr int FB = FBT;
+#pragma unroll
+        for (int h = 0; h < 32; h += FB) {
+          double2 t[FB];
+#pragma unroll
+          for (int jj = 0; jj < FB; ++jj)
+            t[jj] = vp ? Tr<double>::ldT2(reinterpret_cast<const double *>(col) + (int64_t)(h + jj) * ld + tl.start + 2 * lane)
+                       : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int jj = 0; jj < FB; ++jj) {
+            const S x = X::shfl(xr, h + jj);
+            X::fma(acc_a, t[jj].x, x);
+            X::fma(acc_b, t[jj].y, x);
+          }
+        }
+      } else {
 #pragma unroll 8
-      for (int jj = 0; jj < 32; ++jj) step(jj);
+        for (int jj = 0; jj < 32; ++jj) step(jj);
+      }
     } else {
       for (int jj = 0; jj < jn; ++jj) step(jj);
     }
@@ -233,9 +256,18 @@ __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
   if (split && threadIdx.x == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
 }
 
-template <class S>
+template <class S, int FBT = 8>
 __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Tile *__restrict__ tiles) {
-  fwd_tile<S, false>(cx, tiles[blockIdx.y]);
+  fwd_tile<S, false, FBT>(cx, tiles[blockIdx.y]);
+}
+
+// real forward load batching: MHT_FWD_FB=0 (interleaved) | 8 (default) | 16
+inline int fwd_fb() {
+  static int v = [] {
+    const char *e = getenv("MHT_FWD_FB");
+    return e ? atoi(e) : 8;
+  }();
+  return v;
 }
 
 // adjoint input z[i] of a block: f through perm_x (leaf stage), else the group
@@ -315,14 +347,18 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
       if (cbase < cend) {
         for (int q = lane; 2 * q < rn; q += 32) {
           const double z0 = zs[2 * q][0], z1 = zs[2 * q + 1][0];
+          // all CPW column loads issued before their first use (predicated)
+          double2 t[CPW];
+#pragma unroll
+          for (int u = 0; u < CPW; ++u)
+            t[u] = cbase + u < cend
+                       ? Tr<double>::ldT2(reinterpret_cast<const double *>(T) + (int64_t)(cbase + u) * ld + rc + 2 * q)
+                       : make_double2(0.0, 0.0);
 #pragma unroll
           for (int u = 0; u < CPW; ++u) {
-            if (cbase + u < cend) {
-              const double2 t = Tr<double>::ldT2(reinterpret_cast<const double *>(T) + (int64_t)(cbase + u) * ld + rc + 2 * q);
-              double &a = reinterpret_cast<double &>(acc[u][0]);
-              a = ::fma(t.x, z0, a);
-              a = ::fma(t.y, z1, a);
-            }
+            double &a = reinterpret_cast<double &>(acc[u][0]);
+            a = ::fma(t[u].x, z0, a);
+            a = ::fma(t[u].y, z1, a);
           }
         }
       }
@@ -331,14 +367,13 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
         S zv[RB];
 #pragma unroll
         for (int k = 0; k < RB; ++k) zv[k] = zs[i][k];
+        S t[CPW];
 #pragma unroll
-        for (int u = 0; u < CPW; ++u) {
-          if (cbase + u < cend) {
-            const S t = X::ldT(T + (int64_t)(cbase + u) * ld + rc + i);
+        for (int u = 0; u < CPW; ++u) t[u] = cbase + u < cend ? X::ldT(T + (int64_t)(cbase + u) * ld + rc + i) : X::zero();
 #pragma unroll
-            for (int k = 0; k < RB; ++k) X::fmac(acc[u][k], t, zv[k]);
-          }
-        }
+        for (int u = 0; u < CPW; ++u)
+#pragma unroll
+          for (int k = 0; k < RB; ++k) X::fmac(acc[u][k], t[u], zv[k]);
       }
     }
     __syncthreads();
@@ -812,11 +847,19 @@ __host__ __device__ constexpr int ws_mode() {
   return ADJ ? 1 : (sizeof(S) == 8 ? 2 : 0);
 }
 
+// B chunk of the warp-specialised kernel: complex in fragment order (BK x 32
+// slots), real row-major [k][32 + 4] (each row one contiguous 256-byte gather
+// by 16-byte cp.async; the +4 pad makes the fragment reads conflict-free)
+template <class S>
+__host__ __device__ constexpr int ws_b_elems() {
+  return sizeof(S) == 16 ? mm_bk<S>() / 4 * 4 * 32 : mm_bk<S>() * (32 + 4);
+}
+
 template <class S, bool ADJ, bool M3>
 __host__ __device__ constexpr int ws_smem_bytes() {
   // NS x (A tile + B chunk) operand buffers + 2 NS mbarriers + 1 KB to align
   // the stages to the 1024-byte period of the 128-byte TMA swizzle
-  return WS_STAGES * (ws_a_elems<S, ADJ>() + mm_bk<S>() / 4 * 4 * 32) * (int)sizeof(S) + 2 * WS_STAGES * 8 + 1024;
+  return WS_STAGES * (ws_a_elems<S, ADJ>() + ws_b_elems<S>()) * (int)sizeof(S) + 2 * WS_STAGES * 8 + 1024;
 }
 
 template <class S, bool ADJ, bool M3, int MINB>
@@ -836,7 +879,9 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   // column-major [k][m]; adjoint the TMA box [m][k] as written (dense)
   constexpr int AP = ADJ ? BK : MM_BM + 2;  // (mode 0 only)
   constexpr int MODE = ws_mode<S, ADJ>();
-  constexpr int B_CH = KS * NT * 32;
+  constexpr int B_CH = ws_b_elems<S>();
+  constexpr bool BROW = !CPLX;  // real: row-major padded B chunk
+  constexpr int NPB = 32 + 4;
   constexpr int NS = WS_STAGES;
   extern __shared__ __align__(128) unsigned char ws_smem[];
   // stage buffers start at a 1024-byte boundary (shared-space address)
@@ -870,6 +915,10 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
       mbar_init(full + i, 65);   // producer: 1 expect-tx arrival (TMA bytes) + 32 cp.async + 32 plain
       mbar_init(empty + i, AW);  // one arrival per consumer warp
     }
+    // make the initialised barriers visible to the async proxy (the TMA unit
+    // completes transactions on them) before any copy is issued
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
 
@@ -889,17 +938,30 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
       if (ADJ) return from_f_ ? __ldg(cx.perm + B.out_off + k) : k;
       return red_iota ? k : __ldg(cx.idx + B.red_off + k);
     };
+    // real (BROW): lane owns row k = lane of every chunk (BK = 32)
+    auto row_index_r = [&](int kc) -> int {
+      const int k = kbeg + kc * BK + lane;
+      if (k >= kend) return -1;
+      if (ADJ) return from_f_ ? __ldg(cx.perm + B.out_off + k) : k;
+      return red_iota ? k : __ldg(cx.idx + B.red_off + k);
+    };
     int qn[KS];
 #pragma unroll
-    for (int k4 = 0; k4 < KS; ++k4) qn[k4] = nchunks > 0 ? row_index(0, k4) : -1;
+    for (int k4 = 0; k4 < KS; ++k4) qn[k4] = (nchunks > 0 && !BROW) ? row_index(0, k4) : -1;
+    int qrn = (nchunks > 0 && BROW) ? row_index_r(0) : -1;
     for (int kc = 0; kc < nchunks; ++kc) {
       const int slot = kc % NS;
       int q[KS];
 #pragma unroll
       for (int k4 = 0; k4 < KS; ++k4) q[k4] = qn[k4];
+      const int qr = qrn;
       if (kc + 1 < nchunks) {
+        if (BROW) {
+          qrn = row_index_r(kc + 1);
+        } else {
 #pragma unroll
-        for (int k4 = 0; k4 < KS; ++k4) qn[k4] = row_index(kc + 1, k4);
+          for (int k4 = 0; k4 < KS; ++k4) qn[k4] = row_index(kc + 1, k4);
+        }
       }
       mbar_wait(empty + slot, ((kc / NS) & 1) ^ 1);
       const int kb = kbeg + kc * BK;
@@ -940,6 +1002,53 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
         tma_2d_g2s(dA + MM_BM * KH, tmap, (kb + KH) * (int)(sizeof(S) / 8), tl.start, full + slot);
       }
       S *dB = Bs + slot * B_CH;
+      if constexpr (BROW) {
+        // row k = lane: its 32 right-hand sides, contiguous in the workspace
+        // (RHS-fastest) -> 16 x 16-byte cp.async; c / f rows (column-major
+        // user arrays), odd nrhs and a fused diagonal take 8-byte elements
+        S *drow = dB + lane * NPB;
+        const int nv = min(32, cx.nrhs - rhs0);  // valid right-hand sides
+        const S *srow = nullptr;
+        bool contiguous = false;
+        int64_t rstride = 0;  // element stride between right-hand sides otherwise
+        if (qr >= 0) {
+          if (ADJ) {
+            if (from_f_) {
+              srow = static_cast<const S *>(cx.fin) + (int64_t)rhs0 * cx.n + qr;
+              rstride = cx.n;
+            } else {
+              srow = static_cast<const S *>(cx.z) + (B.out_off + qr) * cx.nrhs + rhs0;
+              contiguous = true;
+            }
+          } else {
+            const bool s1 = qr >= B.seg_len[0];
+            const int64_t off = s1 ? B.seg_off[1] + (qr - B.seg_len[0]) : B.seg_off[0] + qr;
+            const int32_t srcsel = s1 ? B.seg_src[1] : B.seg_src[0];
+            if (srcsel == SRC_C) {
+              srow = static_cast<const S *>(cx.c) + (int64_t)rhs0 * cx.m + off;
+              rstride = cx.m;
+            } else {
+              srow = static_cast<const S *>(cx.z) + off * cx.nrhs + rhs0;
+              contiguous = true;
+            }
+          }
+        }
+        if (contiguous && !reg_path && (cx.nrhs & 1) == 0 && cx.b16) {
+#pragma unroll
+          for (int h = 0; h < 16; ++h) cp_async<16>(drow + 2 * h, srow + 2 * h, 2 * h < nv);
+        } else if (!reg_path) {
+          for (int n = 0; n < 32; ++n) {
+            const bool ok = qr >= 0 && n < nv;
+            cp_async<8>(drow + n, ok ? (contiguous ? srow + n : srow + n * rstride) : static_cast<const S *>(cx.z), ok);
+          }
+        } else {
+          for (int n = 0; n < 32; ++n) {
+            const bool ok = qr >= 0 && n < nv;
+            drow[n] = ok ? (ADJ ? (contiguous ? srow[n] : srow[n * rstride]) : in_value<S>(cx, B, qr, rhs0 + n))
+                         : X::zero();
+          }
+        }
+      } else {
 #pragma unroll
       for (int i = 0; i < B_CH / 32; ++i) {
         const int k4 = i / NT, t = i % NT;
@@ -964,6 +1073,7 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
         } else {
           dB[lane + 32 * i] = ok ? (ADJ ? *src : in_value<S>(cx, B, qq, r)) : X::zero();
         }
+      }
       }
       mbar_cp_async_arrive(full + slot);  // completes when this lane's cp.async have landed
       mbar_arrive(full + slot);           // the register-path stores (if any) are done
@@ -1016,7 +1126,7 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
       const double as0 = ar0 + ai0, as1 = ar1 + ai1;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        const S b = Bc[(k4 * NT + t) * 32 + lane];
+        const S b = BROW ? Bc[k * NPB + 8 * t + gid] : Bc[(k4 * NT + t) * 32 + lane];
         if constexpr (!CPLX) {
           dmma(c0[t], ar0, ar1, PL::re(b));
         } else if constexpr (G3) {
@@ -1045,19 +1155,20 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
 // classic kernel (c3: the producer warp's 32 gathers per lane per chunk make
 // WS 1.3-3x slower).  MHT_MMA_WS=0 never, =1 always.
 inline int mma_ws_mode() {
-  static int v = [] {
-    const char *e = getenv("MHT_MMA_WS");
-    if (e && atoi(e) == 0) return 0;
-    if (e && atoi(e) == 1) return 1;
-    return -1;
-  }();
-  return v;
+  const char *e = getenv("MHT_MMA_WS");  // read per launch (debug / A-B within one process)
+  if (e && atoi(e) == 0) return 0;
+  if (e && atoi(e) == 1) return 1;
+  return -1;
 }
 template <class S, bool ADJ>
 inline bool mma_ws() {
+  // real plans never take the warp-specialised kernel: its row-gather
+  // variant showed a rare nondeterministic error on c3 (1 run in 3,
+  // profiles/r01_mma_ws_ab.txt) that is not understood yet
+  if (!Planes<S>::cplx) return false;
   const int mode = mma_ws_mode();
   if (mode >= 0) return mode == 1;
-  return Planes<S>::cplx;
+  return true;
 }
 
 // CTAs per SM the warp-specialised kernel's registers are sized for: 3
@@ -1221,7 +1332,12 @@ template <class S>
 void fwd_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
     const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
-    fwd_kernel<S><<<dim3(1, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
+    if (sizeof(S) == 8 && fwd_fb() == 0)
+      fwd_kernel<S, 0><<<dim3(1, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
+    else if (sizeof(S) == 8 && fwd_fb() == 16)
+      fwd_kernel<S, 16><<<dim3(1, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
+    else
+      fwd_kernel<S><<<dim3(1, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
   }
 }
 
@@ -1229,8 +1345,8 @@ template <class S>
 void adj_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
     const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
-    if (adj_rch() == 1024)
-      adj_kernel<S, 1, 1024><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+    if (adj_rch() == 256)
+      adj_kernel<S, 1, 256><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
     else if (adj_rch() == 512)
       adj_kernel<S, 1, 512><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
     else

@@ -1157,6 +1157,10 @@ Ctx make_ctx(mht_plan *P, int nrhs) {
   cx.fcount = P->d_fcount;
   cx.rdtab = P->d_rdtab;
   cx.tmaps = P->d_tmaps;
+  {
+    const char *e = getenv("MHT_WS_B16");
+    cx.b16 = !(e && atoi(e) == 0);
+  }
   cx.tmaps_f = P->d_tmaps_f;
   cx.diag = P->cur_diag;
   cx.diag_sqrt = P->cur_diag_sqrt;
