@@ -1200,6 +1200,194 @@ void mma_ws_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStr
     mma_ws_launch_t<S, ADJ, M3, 3>(cx, tiles, nt, from_f, st);
 }
 
+// ------------------------------------------------------------------------
+// Real multi-RHS kernel with 16-byte operand copies.  Same tile (64 rows x 32
+// right-hand sides, 4 warps x 16 rows), K chunk 32, two-stage cp.async ring
+// and epilogue as mma_kernel, but both operands are staged as padded dense
+// tiles instead of fragment order, so every copy moves 16 bytes:
+//   A forward  [k][64 + 4]  (row pairs of T's column k),
+//   A adjoint  [m][32 + 4]  (k pairs of T's column tl.start + m),
+//   B          [k][32 + 4]  (a right-hand-side row = 32 contiguous workspace
+//                           entries, 4 threads x 4 copies per row).
+// The +4 pads make the mma fragment loads conflict-free (8-byte slots
+// 4 tig + gid distinct per half warp).  The real kernel was instruction-bound
+// on per-element address math (profiles/r01_ncu_mma_real_c3.txt).
+// ------------------------------------------------------------------------
+constexpr int RB_BK = 32, RB_AP = MM_BM + 4, RB_KP = RB_BK + 4, RB_NP = 32 + 4;
+
+template <bool ADJ>
+__host__ __device__ constexpr int rb_a_elems() {
+  return ADJ ? MM_BM * RB_KP : RB_BK * RB_AP;
+}
+template <bool ADJ>
+__host__ __device__ constexpr int rb_smem_bytes() {
+  return 2 * (rb_a_elems<ADJ>() + RB_BK * RB_NP) * 8;
+}
+
+template <bool ADJ>
+__global__ void __launch_bounds__(MM_THREADS, 4) mma_real_kernel(const Ctx cx, const Tile *__restrict__ tiles,
+                                                                  int from_f) {
+  using S = double;
+  using X = Tr<S>;
+  constexpr int NT = 4, KS = RB_BK / 4, A_CH = rb_a_elems<ADJ>(), B_CH = RB_BK * RB_NP;
+  extern __shared__ __align__(16) unsigned char rb_smem[];
+  S *As = reinterpret_cast<S *>(rb_smem);
+  S *Bs = As + 2 * A_CH;
+
+  const Tile tl = tiles[blockIdx.y];
+  const DevBlock B = cx.blocks[tl.blk];
+  const int rhs0 = blockIdx.x * 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
+  const int64_t ld = B.ld;
+  const int K = ADJ ? B.r_out : B.n_red;
+  const bool ksplit = ADJ && tl.pad >= 0;
+  const int sidx = ksplit ? (tl.pad & 255) : 0;
+  int kbeg = 0, kend = K;
+  if (ksplit) {
+    const int chunk = ((K + B.mks - 1) / B.mks + RB_BK - 1) / RB_BK * RB_BK;
+    kbeg = min(K, sidx * chunk);
+    kend = min(K, kbeg + chunk);
+  }
+  const int nchunks = tl.count > 0 ? (kend - kbeg + RB_BK - 1) / RB_BK : 0;
+  const bool red_iota = (B.flags & F_RED_IOTA) != 0;
+  const bool from_f_ = from_f != 0;
+  const bool reg_path = cx.diag != nullptr;
+  const int nv = min(32, cx.nrhs - rhs0);
+  const bool even = (cx.nrhs & 1) == 0;
+
+  // B row of this thread: row (threadIdx.x >> 2) of each chunk, right-hand
+  // sides 8 (threadIdx.x & 3) .. + 7
+  const int brow = threadIdx.x >> 2, bq = threadIdx.x & 3;
+  auto row_index = [&](int kc) -> int {
+    const int k = kbeg + kc * RB_BK + brow;
+    if (k >= kend) return -1;
+    if (ADJ) return from_f_ ? __ldg(cx.perm + B.out_off + k) : k;
+    return red_iota ? k : __ldg(cx.idx + B.red_off + k);
+  };
+  auto load = [&](int kc, int qr) {
+    const int kb = kbeg + kc * RB_BK;
+    S *dA = As + (kc & 1) * A_CH;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {  // 1024 16-byte A copies / 128 threads
+      const int e = threadIdx.x + MM_THREADS * i;
+      if (!ADJ) {
+        const int k = e >> 5, p = e & 31;  // column k, row pair p
+        const bool ok = 2 * p < tl.count && kb + k < kend;
+        cp_async<16>(dA + k * RB_AP + 2 * p, ok ? T + (int64_t)(kb + k) * ld + tl.start + 2 * p : T, ok);
+      } else {
+        const int m = e >> 4, p = e & 15;  // tile row m (T column), k pair p
+        const bool ok = m < tl.count && kb + 2 * p < kend;
+        cp_async<16>(dA + m * RB_KP + 2 * p, ok ? T + (int64_t)(tl.start + m) * ld + kb + 2 * p : T, ok);
+      }
+    }
+    S *drow = Bs + (kc & 1) * B_CH + brow * RB_NP + 8 * bq;
+    const S *srow = nullptr;
+    bool contiguous = false;
+    int64_t rstride = 0;
+    if (qr >= 0) {
+      if (ADJ) {
+        if (from_f_) {
+          srow = static_cast<const S *>(cx.fin) + (int64_t)rhs0 * cx.n + qr;
+          rstride = cx.n;
+        } else {
+          srow = static_cast<const S *>(cx.z) + (B.out_off + qr) * cx.nrhs + rhs0;
+          contiguous = true;
+        }
+      } else {
+        const bool s1 = qr >= B.seg_len[0];
+        const int64_t off = s1 ? B.seg_off[1] + (qr - B.seg_len[0]) : B.seg_off[0] + qr;
+        if ((s1 ? B.seg_src[1] : B.seg_src[0]) == SRC_C) {
+          srow = static_cast<const S *>(cx.c) + (int64_t)rhs0 * cx.m + off;
+          rstride = cx.m;
+        } else {
+          srow = static_cast<const S *>(cx.z) + off * cx.nrhs + rhs0;
+          contiguous = true;
+        }
+      }
+    }
+    if (reg_path) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int n = 8 * bq + j;
+        const bool ok = qr >= 0 && n < nv;
+        drow[j] = ok ? (ADJ ? (contiguous ? srow[n] : srow[n * rstride]) : in_value<S>(cx, B, qr, rhs0 + n)) : 0.0;
+      }
+    } else if (contiguous && even) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int n = 8 * bq + 2 * j;
+        cp_async<16>(drow + 2 * j, srow + n, qr >= 0 && n < nv);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int n = 8 * bq + j;
+        const bool ok = qr >= 0 && n < nv;
+        cp_async<8>(drow + j, ok ? (contiguous ? srow + n : srow + n * rstride) : static_cast<const S *>(cx.z), ok);
+      }
+    }
+  };
+
+  double c0[NT][4], c1[NT][4], c2[1][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) c0[t][v] = c1[t][v] = 0.0;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) c2[0][v] = 0.0;
+
+  int qn = nchunks > 0 ? row_index(0) : -1;
+  if (nchunks > 0) {
+    load(0, qn);
+    cp_async_commit();
+    if (nchunks > 1) qn = row_index(1);
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  const int m0 = warp * 16 + gid;
+  for (int kc = 0; kc < nchunks; ++kc) {
+    const bool more = kc + 1 < nchunks;
+    if (more) {
+      load(kc + 1, qn);
+      cp_async_commit();
+      if (kc + 2 < nchunks) qn = row_index(kc + 2);
+    }
+    const S *Ac = As + (kc & 1) * A_CH;
+    const S *Bc = Bs + (kc & 1) * B_CH;
+#pragma unroll
+    for (int k4 = 0; k4 < KS; ++k4) {
+      const int k = 4 * k4 + tig;
+      const double a0 = ADJ ? Ac[m0 * RB_KP + k] : Ac[k * RB_AP + m0];
+      const double a1 = ADJ ? Ac[(m0 + 8) * RB_KP + k] : Ac[k * RB_AP + m0 + 8];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) dmma(c0[t], a0, a1, Bc[k * RB_NP + 8 * t + gid]);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  mma_epilogue<S, ADJ, NT, false, 0>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
+}
+
+// real plans: the 16-byte-copy kernel by default, MHT_MMA_REAL=0 for the
+// fragment-order kernel
+inline bool mma_real16() {
+  const char *e = getenv("MHT_MMA_REAL");
+  return !(e && atoi(e) == 0);
+}
+
+template <bool ADJ>
+void mma_real_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
+  constexpr int smem = rb_smem_bytes<ADJ>();
+  static bool attr = [] {
+    cudaFuncSetAttribute(mma_real_kernel<ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return true;
+  }();
+  (void)attr;
+  mma_real_kernel<ADJ><<<dim3((cx.nrhs + 31) / 32, nt), MM_THREADS, smem, st>>>(cx, tiles, from_f);
+}
+
 // Multi-RHS configuration (compile-time variants; default picked from the
 // measurements in profiles/, override with MHT_MMA=4m|3m for experiments).
 inline int mma_variant() {
@@ -1232,7 +1420,9 @@ void mma_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cuda
   for (int t0 = 0; t0 < ntiles; t0 += 65535) {
     const int nt = ntiles - t0 < 65535 ? ntiles - t0 : 65535;
     const int v = Planes<S>::cplx ? mma_variant() : 0;
-    if (cx.nrhs >= 32 && mma_ws<S, ADJ>()) {
+    if (!Planes<S>::cplx && cx.nrhs >= 32 && mma_real16()) {
+      mma_real_launch<ADJ>(cx, tiles + t0, nt, from_f, st);
+    } else if (cx.nrhs >= 32 && mma_ws<S, ADJ>()) {
       if (v >= 1)
         mma_ws_launch<S, ADJ, true>(cx, tiles + t0, nt, from_f, st);
       else
