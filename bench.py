@@ -407,14 +407,17 @@ def main():
         kname = (f"persist_kernel {dkind} nrhs=1 (all stages in one cooperative launch)" if dn == args.steps
                  else f"{dkind}_kernel nrhs=1")
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "algorithmic_bytes_per_launch": alg,
+                "frac": achieved / peaks["hbm_gbs"], "frac_of_nominal_8TBs": achieved / 8000.0,
+                "traffic": traffic, "algorithmic_bytes_per_launch": alg,
                 "kernel": kname, "peak_source": peaks["hbm_src"]}
     else:
         # the multi-RHS stages run on the FP64 tensor pipe (DMMA): its own measured peak
         alg = (8 if P.is_complex else 2) * entries * dr / (dn / args.steps)
         achieved = alg / (per_launch_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["dmma_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["dmma_tflops"], "traffic": traffic, "algorithmic_flops_per_launch": alg,
+                "frac": achieved / peaks["dmma_tflops"],
+                "frac_of_nominal": achieved / (148 * 64 * 2 * 1.965e9 / 1e12),  # 37.2 TF: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz
+                "traffic": traffic, "algorithmic_flops_per_launch": alg,
                 "kernel": (f"{'mma_ws_kernel' if P.is_complex else 'mma_kernel'} {dkind} nrhs={dr} "
                            f"(DMMA m16n8k4 f64{', TMA + warp-specialised' if P.is_complex else ''})"),
                 "peak_source": peaks["dmma_src"]}
