@@ -13,9 +13,13 @@ method's arithmetic.
 * P1 finite elements: cotangent stiffness K, lumped (barycentric) mass M.
 * Lowest m eigenpairs of K phi = lambda M phi, M-orthonormal
   (Phi^T M Phi = I), each eigenvector's sign fixed so its largest-magnitude
-  entry is positive (reading A11).  Computed densely through
-  M^{-1/2} K M^{-1/2} (torch.linalg.eigh on a GPU when one is present, else
-  scipy).
+  entry is positive (reading A11).  Computed through A = M^{-1/2} K M^{-1/2}:
+  on a GPU for n > 8192 by Chebyshev-filtered subspace iteration on the
+  sparse A (`chebyshev_subspace_eigs`; the dense eigh of the 32,768^2 matrix
+  took ~650 s), otherwise by a dense eigh (torch on a GPU, else scipy).
+  Eigenvectors inside a degenerate eigenspace are not unique; any
+  M-orthonormal basis of it is a valid input (the oracle and the plan read
+  the same stored Phi).
 """
 from __future__ import annotations
 
@@ -73,6 +77,59 @@ def cotan_fem(V: np.ndarray, F: np.ndarray, n: int | None = None):
     return K.tocsr(), mass
 
 
+def chebyshev_subspace_eigs(K, mass, m: int, device=None, oversample: int | None = None, degree: int = 24,
+                            tol: float = 1e-12, maxit: int = 60, seed: int = 0):
+    """Lowest m eigenpairs of K phi = lambda M phi (M = diag(mass)) by
+    Chebyshev-filtered subspace iteration on A = M^-1/2 K M^-1/2 (sparse).
+
+    Block of p = m + oversample vectors; each sweep applies the degree-d
+    Chebyshev polynomial that damps [a, b] (a = the block's largest Ritz
+    value, b = a Gershgorin upper bound of the spectrum), re-orthonormalises
+    (QR) and does a Rayleigh-Ritz step; stops when every one of the m wanted
+    residuals ||A x - theta x|| <= tol * b.  Returns (lam (m,), Q (n, m))
+    with A Q = Q diag(lam), Q orthonormal.  torch on `device` (a GPU here:
+    a dense eigh of a 32,768^2 matrix takes ~10 minutes)."""
+    import torch
+
+    n = K.shape[0]
+    p = m + (oversample if oversample is not None else max(64, m // 8))
+    s = 1.0 / np.sqrt(mass)
+    A = (K.multiply(s[:, None]).multiply(s[None, :])).tocsr()
+    A = 0.5 * (A + A.T)
+    A = A.tocsr()
+    b = float(np.max(np.asarray(abs(A).sum(axis=1)).ravel())) * 1.01  # Gershgorin upper bound
+    dev = torch.device(device) if device is not None else torch.device("cpu")
+    At = torch.sparse_csr_tensor(torch.from_numpy(A.indptr.astype(np.int64)), torch.from_numpy(A.indices.astype(np.int64)),
+                                 torch.from_numpy(A.data), size=A.shape, dtype=torch.float64).to(dev)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    X = torch.randn(n, p, generator=g, dtype=torch.float64).to(dev)
+    X, _ = torch.linalg.qr(X)
+
+    def rayleigh_ritz(X):
+        AX = At @ X
+        H = X.T @ AX
+        w, S = torch.linalg.eigh(0.5 * (H + H.T))
+        return w, X @ S, AX @ S
+
+    w, X, AX = rayleigh_ritz(X)
+    for it in range(maxit):
+        res = torch.linalg.vector_norm(AX[:, :m] - X[:, :m] * w[None, :m], dim=0)
+        if float(res.max()) <= tol * b:
+            break
+        a = float(w[-1])  # damp everything above the block's top Ritz value
+        e, c = (b - a) / 2.0, (b + a) / 2.0
+        Y0 = X
+        Y1 = (At @ X - c * X) / e
+        for _ in range(2, degree + 1):
+            Y2 = 2.0 * (At @ Y1 - c * Y1) / e - Y0
+            Y0, Y1 = Y1, Y2
+        X, _ = torch.linalg.qr(Y1)
+        w, X, AX = rayleigh_ritz(X)
+    lam = w[:m].cpu().numpy()
+    Q = X[:, :m].cpu().numpy()
+    return lam, Q
+
+
 def _eigh_lowest(A: np.ndarray, m: int):
     """Lowest m eigenpairs of a dense symmetric matrix (GPU if available)."""
     try:
@@ -92,14 +149,30 @@ def _eigh_lowest(A: np.ndarray, m: int):
     return sl.eigh(A, subset_by_index=[0, m - 1], driver="evr")
 
 
-def mesh_eigenbasis(V, F, m: int):
-    """(lam (m,), Phi (n, m) float64 M-orthonormal, mass (n,), K csr)."""
+def mesh_eigenbasis(V, F, m: int, method: str = "auto"):
+    """(lam (m,), Phi (n, m) float64 M-orthonormal, mass (n,), K csr).
+
+    method: "dense" (eigh of the dense M^-1/2 K M^-1/2), "chebyshev"
+    (filtered subspace iteration, sparse), "auto" = chebyshev on a GPU for
+    n > 8192, else dense."""
     n = V.shape[0]
     K, mass = cotan_fem(V, F)
     s = 1.0 / np.sqrt(mass)
-    A = (K.multiply(s[:, None]).multiply(s[None, :])).toarray()
-    A = 0.5 * (A + A.T)
-    lam, Q = _eigh_lowest(A, m)
+    if method == "auto":
+        try:
+            import torch
+
+            method = "chebyshev" if (n > 8192 and torch.cuda.is_available()) else "dense"
+        except Exception:
+            method = "dense"
+    if method == "chebyshev":
+        import torch
+
+        lam, Q = chebyshev_subspace_eigs(K, mass, m, device="cuda" if torch.cuda.is_available() else None)
+    else:
+        A = (K.multiply(s[:, None]).multiply(s[None, :])).toarray()
+        A = 0.5 * (A + A.T)
+        lam, Q = _eigh_lowest(A, m)
     Phi = Q * s[:, None]
     # sign convention: largest-magnitude entry positive (reading A11)
     j = np.argmax(np.abs(Phi), axis=0)
@@ -116,7 +189,7 @@ def torus_workload_inputs(nu=256, nv=128, m=2048, cache_dir=None):
     cache_dir = cache_dir or os.environ.get("MHT_PLAN_DIR") or (
         "/dev/shm/mht_plans" if os.path.isdir("/dev/shm") else "/tmp/mht_plans")
     os.makedirs(cache_dir, exist_ok=True)
-    path = os.path.join(cache_dir, f"torus_{nu}x{nv}_m{m}_v1.npz")
+    path = os.path.join(cache_dir, f"torus_{nu}x{nv}_m{m}_v2.npz")
     if os.path.exists(path):
         d = np.load(path)
         return V, F, d["lam"], d["Phi"], d["mass"]
