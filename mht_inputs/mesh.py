@@ -78,7 +78,7 @@ def cotan_fem(V: np.ndarray, F: np.ndarray, n: int | None = None):
 
 
 def chebyshev_subspace_eigs(K, mass, m: int, device=None, oversample: int | None = None, degree: int = 24,
-                            tol: float = 1e-12, maxit: int = 60, seed: int = 0):
+                            tol: float = 1e-12, maxit: int = 200, seed: int = 0, info: dict | None = None):
     """Lowest m eigenpairs of K phi = lambda M phi (M = diag(mass)) by
     Chebyshev-filtered subspace iteration on A = M^-1/2 K M^-1/2 (sparse).
 
@@ -112,9 +112,13 @@ def chebyshev_subspace_eigs(K, mass, m: int, device=None, oversample: int | None
         return w, X @ S, AX @ S
 
     w, X, AX = rayleigh_ritz(X)
+    converged = False
     for it in range(maxit):
         res = torch.linalg.vector_norm(AX[:, :m] - X[:, :m] * w[None, :m], dim=0)
+        if info is not None:
+            info["iterations"], info["max_residual"], info["bound"] = it, float(res.max()), b
         if float(res.max()) <= tol * b:
+            converged = True
             break
         a = float(w[-1])  # damp everything above the block's top Ritz value
         e, c = (b - a) / 2.0, (b + a) / 2.0
@@ -125,6 +129,9 @@ def chebyshev_subspace_eigs(K, mass, m: int, device=None, oversample: int | None
             Y0, Y1 = Y1, Y2
         X, _ = torch.linalg.qr(Y1)
         w, X, AX = rayleigh_ritz(X)
+    if not converged:
+        raise RuntimeError(f"chebyshev_subspace_eigs: no convergence in {maxit} sweeps "
+                           f"(max residual {float(res.max()):.3e} > {tol * b:.3e})")
     lam = w[:m].cpu().numpy()
     Q = X[:, :m].cpu().numpy()
     return lam, Q

@@ -27,6 +27,15 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// Programmatic dependent launch (the nrhs = 1 stage kernels): a CTA lets the
+// next stage's grid start launching at once, prefetches its own factor lines
+// into L2 (the factors never depend on the previous stage), and only then
+// waits for the previous grid's results.  griddepcontrol.wait is a no-op for
+// a launch without the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 template <class S>
 struct Tr;
 
@@ -258,7 +267,26 @@ __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
 
 template <class S, int FBT = 8>
 __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Tile *__restrict__ tiles) {
-  fwd_tile<S, false, FBT>(cx, tiles[blockIdx.y]);
+  const Tile tl = tiles[blockIdx.y];
+  pdl_trigger();
+  {
+    // L2 prefetch of this warp's first 32 factor columns (the tile's rows)
+    const DevBlock &B = cx.blocks[tl.blk];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int jbeg = 0;
+    if (tl.pad >= 0) {
+      const int ks = B.pad;
+      jbeg = (tl.pad & 255) * ((((B.n_red + ks - 1) / ks) + 31) & ~31);
+    }
+    const int j = jbeg + warp * 32 + lane;
+    if (j < B.n_red) {
+      const char *col = reinterpret_cast<const char *>(static_cast<const S *>(cx.coef) + B.coef_off + (int64_t)j * B.ld +
+                                                       tl.start);
+      for (int o = 0; o < tl.count * (int)sizeof(S); o += 128) prefetch_l2(col + o);
+    }
+  }
+  pdl_wait();
+  fwd_tile<S, false, FBT>(cx, tl);
 }
 
 // real forward load batching: MHT_FWD_FB=0 (interleaved) | 8 (default) | 16
@@ -437,7 +465,23 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
 template <class S, int RB, int RCH = ADJ_RCH>
 __global__ void __launch_bounds__(ADJ_THREADS, 7) adj_kernel(const Ctx cx, const Tile *__restrict__ tiles,
                                                              int from_f) {
-  adj_tile<S, RB, false, RCH>(cx, tiles[blockIdx.y], from_f, blockIdx.x * RB);
+  const Tile tl = tiles[blockIdx.y];
+  pdl_trigger();
+  {
+    // L2 prefetch of the first 1 KB of each of this CTA's factor columns
+    const DevBlock &B = cx.blocks[tl.blk];
+    const int t = threadIdx.x;
+    const int col = tl.start + (t >> 3), line = t & 7;
+    if ((t >> 3) < tl.count) {
+      int rbeg = 0;
+      if (tl.pad >= 0) rbeg = (tl.pad & 255) * ((((B.r_out + B.pad2 - 1) / B.pad2) + 31) & ~31);
+      const int64_t off = (int64_t)col * B.ld + rbeg;
+      const char *p = reinterpret_cast<const char *>(static_cast<const S *>(cx.coef) + B.coef_off + off);
+      if (line * 128 < (B.r_out - rbeg) * (int)sizeof(S)) prefetch_l2(p + line * 128);
+    }
+  }
+  pdl_wait();
+  adj_tile<S, RB, false, RCH>(cx, tl, from_f, blockIdx.x * RB);
 }
 
 // rows of z staged per pass: MHT_ADJ_RCH=512|1024 (experiments), default ADJ_RCH
@@ -1462,7 +1506,31 @@ __device__ __forceinline__ void reduce_piece(const Ctx &cx, const Piece p, const
 template <class S>
 __global__ void __launch_bounds__(256) reduce_kernel(const Ctx cx, const Piece *__restrict__ pieces,
                                                      const int64_t *__restrict__ rd) {
+  pdl_trigger();
+  pdl_wait();
   reduce_piece<S, false>(cx, pieces[blockIdx.x], rd, blockIdx.y, gridDim.y);  // y: slices of wide pieces
+}
+
+// launch with the programmatic-stream-serialisation attribute (PDL) unless
+// MHT_PDL=0; read per launch (graphs capture the attribute as a programmatic
+// edge)
+inline bool pdl_on() {
+  const char *e = getenv("MHT_PDL");
+  return !(e && atoi(e) == 0);
+}
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 // ------------------------------------------------------------------------
@@ -1522,12 +1590,13 @@ template <class S>
 void fwd_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
     const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
+    const Tile *tp = tiles + t0;
     if (sizeof(S) == 8 && fwd_fb() == 0)
-      fwd_kernel<S, 0><<<dim3(1, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
+      launch_pdl(fwd_kernel<S, 0>, dim3(1, nt), dim3(FWD_THREADS), st, cx, tp);
     else if (sizeof(S) == 8 && fwd_fb() == 16)
-      fwd_kernel<S, 16><<<dim3(1, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
+      launch_pdl(fwd_kernel<S, 16>, dim3(1, nt), dim3(FWD_THREADS), st, cx, tp);
     else
-      fwd_kernel<S><<<dim3(1, nt), FWD_THREADS, 0, st>>>(cx, tiles + t0);
+      launch_pdl(fwd_kernel<S>, dim3(1, nt), dim3(FWD_THREADS), st, cx, tp);
   }
 }
 
@@ -1535,12 +1604,13 @@ template <class S>
 void adj_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
     const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
+    const Tile *tp = tiles + t0;
     if (adj_rch() == 256)
-      adj_kernel<S, 1, 256><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+      launch_pdl(adj_kernel<S, 1, 256>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
     else if (adj_rch() == 512)
-      adj_kernel<S, 1, 512><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+      launch_pdl(adj_kernel<S, 1, 512>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
     else
-      adj_kernel<S, 1><<<dim3(1, nt), ADJ_THREADS, 0, st>>>(cx, tiles + t0, from_f);
+      launch_pdl(adj_kernel<S, 1>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
   }
 }
 
@@ -1657,9 +1727,9 @@ void launch_reduce(bool is_complex, const Ctx &ctx, const Piece *pieces, const i
   // a piece is <= 1024 entries x nrhs values: give every 2048 values a CTA
   const int ny = ctx.nrhs <= 2 ? 1 : (ctx.nrhs / 2 < 64 ? ctx.nrhs / 2 : 64);
   if (is_complex)
-    reduce_kernel<double2><<<dim3(npieces, ny), 256, 0, (cudaStream_t)stream>>>(ctx, pieces, rd);
+    launch_pdl(reduce_kernel<double2>, dim3(npieces, ny), dim3(256), (cudaStream_t)stream, ctx, pieces, rd);
   else
-    reduce_kernel<double><<<dim3(npieces, ny), 256, 0, (cudaStream_t)stream>>>(ctx, pieces, rd);
+    launch_pdl(reduce_kernel<double>, dim3(npieces, ny), dim3(256), (cudaStream_t)stream, ctx, pieces, rd);
 }
 
 }  // namespace mht
