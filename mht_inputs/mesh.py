@@ -15,8 +15,9 @@ method's arithmetic.
   (Phi^T M Phi = I), each eigenvector's sign fixed so its largest-magnitude
   entry is positive (reading A11).  Computed through A = M^{-1/2} K M^{-1/2}:
   on a GPU for n > 8192 by Chebyshev-filtered subspace iteration on the
-  sparse A (`chebyshev_subspace_eigs`; the dense eigh of the 32,768^2 matrix
-  took ~650 s), otherwise by a dense eigh (torch on a GPU, else scipy).
+  sparse A (`chebyshev_subspace_eigs`, degree-64 filters: the noisy mesh's
+  spectrum reaches ~4e5, degree 24 stalls; the dense eigh of the 32,768^2
+  matrix took ~650 s), otherwise by a dense eigh (torch on a GPU, else scipy).
   Eigenvectors inside a degenerate eigenspace are not unique; any
   M-orthonormal basis of it is a valid input (the oracle and the plan read
   the same stored Phi).
@@ -77,7 +78,7 @@ def cotan_fem(V: np.ndarray, F: np.ndarray, n: int | None = None):
     return K.tocsr(), mass
 
 
-def chebyshev_subspace_eigs(K, mass, m: int, device=None, oversample: int | None = None, degree: int = 24,
+def chebyshev_subspace_eigs(K, mass, m: int, device=None, oversample: int | None = None, degree: int = 64,
                             tol: float = 1e-12, maxit: int = 200, seed: int = 0, info: dict | None = None):
     """Lowest m eigenpairs of K phi = lambda M phi (M = diag(mass)) by
     Chebyshev-filtered subspace iteration on A = M^-1/2 K M^-1/2 (sparse).
@@ -196,7 +197,7 @@ def torus_workload_inputs(nu=256, nv=128, m=2048, cache_dir=None):
     cache_dir = cache_dir or os.environ.get("MHT_PLAN_DIR") or (
         "/dev/shm/mht_plans" if os.path.isdir("/dev/shm") else "/tmp/mht_plans")
     os.makedirs(cache_dir, exist_ok=True)
-    path = os.path.join(cache_dir, f"torus_{nu}x{nv}_m{m}_v2.npz")
+    path = os.path.join(cache_dir, f"torus_{nu}x{nv}_m{m}_v3.npz")
     if os.path.exists(path):
         d = np.load(path)
         return V, F, d["lam"], d["Phi"], d["mass"]

@@ -73,7 +73,7 @@ def build_workload_plan(w: mi.Workload, path: str, workers=None, log=print, prec
 
 
 # bump when the builders' numerics change so cached plans are never reused across versions
-BUILDER_VERSION = 3
+BUILDER_VERSION = 4
 
 
 def plan_cache_path(w: mi.Workload, root: str | None = None) -> str:
