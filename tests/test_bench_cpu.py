@@ -20,3 +20,25 @@ def test_reference_arm_json(tmp_path):
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["steps"] == 2 and d["warmup"] == 1
+
+
+def test_reference_arm_under_torchrun_two_ranks(tmp_path):
+    """Launched like the driver's N > 1 runs (torchrun, 127.0.0.1): rank 0
+    alone runs the reference arm and prints one JSON line; the other rank
+    exits 0 without work (gloo on CPU here, NCCL on GPUs)."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, MHT_PLAN_DIR=str(tmp_path), CUDA_VISIBLE_DEVICES="")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--impl", "reference",
+                        "--gpus", "2", "--workload", "c1", "--builder", "cpu", "--steps", "1", "--warmup", "1"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
