@@ -628,9 +628,16 @@ __device__ __forceinline__ void mma_epilogue(const Ctx &cx, const Tile &tl, cons
       }
     }
   }
-  if (ADJ && tl.start == 0 && sidx == 0 && B.n_skel > 0) {
-    for (int e = threadIdx.x; e < B.n_skel * NRT; e += MM_THREADS) {
-      const int i = e % B.n_skel, r = rhs0 + e / B.n_skel;
+  if (ADJ && sidx == 0 && B.n_skel > 0) {
+    // skeleton part w[skel[i]] = z[i], spread over the block's column tiles
+    // (tile j copies rows [j c, (j + 1) c)); a block without redundant
+    // columns (COPY) has one tile that copies everything
+    const int ntl = B.n_red > 0 ? (B.n_red + MMA_COLS - 1) / MMA_COLS : 1;
+    const int chunk = (B.n_skel + ntl - 1) / ntl;
+    const int i0 = (tl.start / MMA_COLS) * chunk, i1 = min(B.n_skel, i0 + chunk);
+    const int ni = i1 - i0;
+    for (int e = threadIdx.x; e < ni * NRT; e += MM_THREADS) {
+      const int i = i0 + e / NRT, r = rhs0 + e % NRT;  // RHS fastest: contiguous 32-wide rows
       if (r >= cx.nrhs) continue;
       const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
       static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = adj_in<S>(cx, B, i, r, from_f != 0);

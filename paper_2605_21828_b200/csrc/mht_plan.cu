@@ -726,7 +726,8 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
     } else {
       for (int c0 = 0; c0 < D.n_red; c0 += MMA_COLS) {
         int cnt = std::min(MMA_COLS, D.n_red - c0);
-        amt[s].push_back({(int64_t)cnt * (D.r_out + 4) + (c0 == 0 ? D.n_skel : 0), Tile{i, c0, cnt, -1}});
+        const int ntl = (D.n_red + MMA_COLS - 1) / MMA_COLS;  // the skeleton copy is spread over the tiles
+        amt[s].push_back({(int64_t)cnt * (D.r_out + 4) + (D.n_skel + ntl - 1) / ntl, Tile{i, c0, cnt, -1}});
       }
     }
     if (D.n_red == 0) {
