@@ -886,16 +886,18 @@ constexpr int WS_THREADS = MM_THREADS + 32;
 // row-major [m][k] with BKP = BK + 4; chosen so a warp's A-fragment loads hit
 // distinct banks (16-byte slots 2 tig + gid / 4 gid + tig distinct mod 8 per
 // quarter warp; 8-byte slots distinct mod 16 per half warp)
-template <class S, bool ADJ>
+template <class S, bool ADJ, int FM = 0>
 __host__ __device__ constexpr int ws_a_elems() {
-  return (ADJ || sizeof(S) == 8) ? MM_BM * mm_bk<S>() : mm_bk<S>() * (MM_BM + 2);
+  return (ADJ || sizeof(S) == 8 || FM == 3) ? MM_BM * mm_bk<S>() : mm_bk<S>() * (MM_BM + 2);
 }
 // A-tile layout / row mapping of the warp-specialised kernel: 0 padded
 // column-major by 1-D bulk copies (complex forward), 1 swizzled [half][m][k]
 // by 2-D TMA (adjoint), 2 swizzled [quad][k][16 rows] by 2-D TMA (real forward)
-template <class S, bool ADJ>
+// FM (complex forward): 0 = padded 1-D bulk copies, 3 = swizzled [q][k][8 rows]
+// by eight 2-D TMA requests (fragment rows permuted as in mode 1)
+template <class S, bool ADJ, int FM = 0>
 __host__ __device__ constexpr int ws_mode() {
-  return ADJ ? 1 : (sizeof(S) == 8 ? 2 : 0);
+  return ADJ ? 1 : (sizeof(S) == 8 ? 2 : FM);
 }
 
 // B chunk of the warp-specialised kernel: complex in fragment order (BK x 32
@@ -906,14 +908,14 @@ __host__ __device__ constexpr int ws_b_elems() {
   return sizeof(S) == 16 ? mm_bk<S>() / 4 * 4 * 32 : mm_bk<S>() * (32 + 4);
 }
 
-template <class S, bool ADJ, bool M3>
+template <class S, bool ADJ, bool M3, int FM = 0>
 __host__ __device__ constexpr int ws_smem_bytes() {
   // NS x (A tile + B chunk) operand buffers + 2 NS mbarriers + 1 KB to align
   // the stages to the 1024-byte period of the 128-byte TMA swizzle
-  return WS_STAGES * (ws_a_elems<S, ADJ>() + ws_b_elems<S>()) * (int)sizeof(S) + 2 * WS_STAGES * 8 + 1024;
+  return WS_STAGES * (ws_a_elems<S, ADJ, FM>() + ws_b_elems<S>()) * (int)sizeof(S) + 2 * WS_STAGES * 8 + 1024;
 }
 
-template <class S, bool ADJ, bool M3, int MINB>
+template <class S, bool ADJ, bool M3, int MINB, int FM = 0>
 __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, const Tile *__restrict__ tiles,
                                                                   int from_f) {
   using X = Tr<S>;
@@ -925,11 +927,11 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   constexpr int BK = mm_bk<S>();
   constexpr int KS = BK / 4;
   constexpr int AW = MM_BM / 16;
-  constexpr int A_CH = ws_a_elems<S, ADJ>();
+  constexpr int A_CH = ws_a_elems<S, ADJ, FM>();
   // leading dimension of the factor tile in shared memory: forward padded
   // column-major [k][m]; adjoint the TMA box [m][k] as written (dense)
   constexpr int AP = ADJ ? BK : MM_BM + 2;  // (mode 0 only)
-  constexpr int MODE = ws_mode<S, ADJ>();
+  constexpr int MODE = ws_mode<S, ADJ, FM>();
   constexpr int B_CH = ws_b_elems<S>();
   constexpr bool BROW = !CPLX;  // real: row-major padded B chunk
   constexpr int NPB = 32 + 4;
@@ -1021,7 +1023,16 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
       // factor tile by TMA bulk copies (16-byte multiples: the real layout has
       // even ld and a zero pad row, so an odd length rounds up into it)
       constexpr int EV = sizeof(S) == 8 ? 2 : 1;
-      if (MODE == 2) {
+      if (MODE == 3) {
+        if (lane == 0) {
+          // complex forward: 64 x BK tile as eight 2-D TMA requests of 8 rows
+          // (128 B) x BK columns, 128-byte swizzled, past-the-block zero-filled
+          const void *tmap = static_cast<const unsigned char *>(cx.tmaps_f) + (size_t)tl.blk * 128;
+          mbar_arrive_expect_tx(full + slot, (unsigned)(MM_BM * BK * sizeof(S)));
+#pragma unroll
+          for (int q8 = 0; q8 < 8; ++q8) tma_2d_g2s(dA + q8 * BK * 8, tmap, 2 * (tl.start + 8 * q8), kb, full + slot);
+        }
+      } else if (MODE == 2) {
         if (lane == 0) {
           // real forward: the 64 x BK tile as four 2-D TMA requests of 16 rows
           // (128 B) x BK columns, 128-byte swizzled, past-the-block zero-filled
@@ -1148,12 +1159,18 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
     mbar_wait(full + slot, (kc / NS) & 1);
     const S *Ac = As + slot * A_CH;
     const S *Bc = Bs + slot * B_CH;
-    const int m0 = warp * 16 + tile_row<S, MODE>(gid), m1 = warp * 16 + tile_row<S, MODE>(gid + 8);
+    constexpr int RMODE = MODE == 3 ? 1 : MODE;  // row permutation
+    const int m0 = warp * 16 + tile_row<S, RMODE>(gid), m1 = warp * 16 + tile_row<S, RMODE>(gid + 8);
 #pragma unroll
     for (int k4 = 0; k4 < KS; ++k4) {
       const int k = 4 * k4 + tig;
       S a0, a1;
-      if constexpr (MODE == 2) {
+      if constexpr (MODE == 3) {
+        // swizzled [q][k][8 rows]: 16-byte chunk (row m & 7) of row k at (m & 7) ^ (k & 7)
+        const unsigned char *ab = reinterpret_cast<const unsigned char *>(Ac) + k * 128;
+        a0 = *reinterpret_cast<const S *>(ab + (m0 >> 3) * (BK * 128) + (((m0 & 7) ^ (k & 7)) << 4));
+        a1 = *reinterpret_cast<const S *>(ab + (m1 >> 3) * (BK * 128) + (((m1 & 7) ^ (k & 7)) << 4));
+      } else if constexpr (MODE == 2) {
         // swizzled [quad][k][16 rows]: 16-byte chunk c of row k sits at c ^ (k & 7)
         const unsigned char *ab = reinterpret_cast<const unsigned char *>(Ac) + k * 128;
         const int mm0 = m0 & 15, mm1 = m1 & 15;
@@ -1197,7 +1214,8 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   }
   // all consumer warps are past their last read of the operand buffers
   consumer_sync<1>();
-  mma_epilogue<S, ADJ, NT, M3, 1, MODE>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
+  constexpr int RMODE_EPI = MODE == 3 ? 1 : MODE;
+  mma_epilogue<S, ADJ, NT, M3, 1, RMODE_EPI>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
 }
 
 // Which multi-RHS launches use the warp-specialised TMA kernel
@@ -1232,23 +1250,34 @@ inline int mma_ws_minb() {
   return v;
 }
 
-template <class S, bool ADJ, bool M3, int MINB>
+template <class S, bool ADJ, bool M3, int MINB, int FM>
 void mma_ws_launch_t(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
-  constexpr int smem = ws_smem_bytes<S, ADJ, M3>();
+  constexpr int smem = ws_smem_bytes<S, ADJ, M3, FM>();
   static bool attr = [] {
-    cudaFuncSetAttribute(mma_ws_kernel<S, ADJ, M3, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(mma_ws_kernel<S, ADJ, M3, MINB, FM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)attr;
-  mma_ws_kernel<S, ADJ, M3, MINB><<<dim3((cx.nrhs + 31) / 32, nt), WS_THREADS, smem, st>>>(cx, tiles, from_f);
+  mma_ws_kernel<S, ADJ, M3, MINB, FM><<<dim3((cx.nrhs + 31) / 32, nt), WS_THREADS, smem, st>>>(cx, tiles, from_f);
+}
+
+// complex forward A tile: MHT_WS_FMODE=3 (2-D TMA, swizzled) | 0 (1-D bulk
+// copies, padded; default)
+inline int ws_fmode() {
+  const char *e = getenv("MHT_WS_FMODE");
+  return (e && atoi(e) == 3) ? 3 : 0;
 }
 
 template <class S, bool ADJ, bool M3>
 void mma_ws_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
-  if (mma_ws_minb() == 2)
-    mma_ws_launch_t<S, ADJ, M3, 2>(cx, tiles, nt, from_f, st);
-  else
-    mma_ws_launch_t<S, ADJ, M3, 3>(cx, tiles, nt, from_f, st);
+  const bool f3 = !ADJ && Planes<S>::cplx && ws_fmode() == 3;
+  if (mma_ws_minb() == 2) {
+    if (f3) mma_ws_launch_t<S, ADJ, M3, 2, 3>(cx, tiles, nt, from_f, st);
+    else mma_ws_launch_t<S, ADJ, M3, 2, 0>(cx, tiles, nt, from_f, st);
+  } else {
+    if (f3) mma_ws_launch_t<S, ADJ, M3, 3, 3>(cx, tiles, nt, from_f, st);
+    else mma_ws_launch_t<S, ADJ, M3, 3, 0>(cx, tiles, nt, from_f, st);
+  }
 }
 
 // ------------------------------------------------------------------------
@@ -1264,26 +1293,30 @@ void mma_ws_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStr
 // 4 tig + gid distinct per half warp).  The real kernel was instruction-bound
 // on per-element address math (profiles/r01_ncu_mma_real_c3.txt).
 // ------------------------------------------------------------------------
-constexpr int RB_BK = 32, RB_AP = MM_BM + 4, RB_KP = RB_BK + 4, RB_NP = 32 + 4;
+constexpr int RB_AP = MM_BM + 4, RB_NP = 32 + 4;
 
-template <bool ADJ>
+template <bool ADJ, int BKT>
 __host__ __device__ constexpr int rb_a_elems() {
-  return ADJ ? MM_BM * RB_KP : RB_BK * RB_AP;
+  return ADJ ? MM_BM * (BKT + 4) : BKT * RB_AP;
 }
-template <bool ADJ>
+template <bool ADJ, int BKT, int NSTG>
 __host__ __device__ constexpr int rb_smem_bytes() {
-  return 2 * (rb_a_elems<ADJ>() + RB_BK * RB_NP) * 8;
+  return NSTG * (rb_a_elems<ADJ, BKT>() + BKT * RB_NP) * 8;
 }
 
-template <bool ADJ>
+template <bool ADJ, int BKT, int NSTG>
 __global__ void __launch_bounds__(MM_THREADS, 4) mma_real_kernel(const Ctx cx, const Tile *__restrict__ tiles,
                                                                   int from_f) {
   using S = double;
   using X = Tr<S>;
-  constexpr int NT = 4, KS = RB_BK / 4, A_CH = rb_a_elems<ADJ>(), B_CH = RB_BK * RB_NP;
+  constexpr int RB_BK = BKT, RB_KP = BKT + 4;
+  constexpr int NT = 4, KS = RB_BK / 4, A_CH = rb_a_elems<ADJ, BKT>(), B_CH = RB_BK * RB_NP;
+  constexpr int APT = RB_BK * MM_BM / 2 / MM_THREADS;     // 16-byte A copies per thread per chunk
+  constexpr int TPR = MM_THREADS / RB_BK;                 // threads per B row
+  constexpr int RPT = 32 / TPR;                           // right-hand sides per thread
   extern __shared__ __align__(16) unsigned char rb_smem[];
   S *As = reinterpret_cast<S *>(rb_smem);
-  S *Bs = As + 2 * A_CH;
+  S *Bs = As + NSTG * A_CH;
 
   const Tile tl = tiles[blockIdx.y];
   const DevBlock B = cx.blocks[tl.blk];
@@ -1310,7 +1343,7 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_real_kernel(const Ctx cx, c
 
   // B row of this thread: row (threadIdx.x >> 2) of each chunk, right-hand
   // sides 8 (threadIdx.x & 3) .. + 7
-  const int brow = threadIdx.x >> 2, bq = threadIdx.x & 3;
+  const int brow = threadIdx.x / TPR, bq = threadIdx.x % TPR;
   auto row_index = [&](int kc) -> int {
     const int k = kbeg + kc * RB_BK + brow;
     if (k >= kend) return -1;
@@ -1319,21 +1352,21 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_real_kernel(const Ctx cx, c
   };
   auto load = [&](int kc, int qr) {
     const int kb = kbeg + kc * RB_BK;
-    S *dA = As + (kc & 1) * A_CH;
+    S *dA = As + (kc % NSTG) * A_CH;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {  // 1024 16-byte A copies / 128 threads
+    for (int i = 0; i < APT; ++i) {  // BK x 32 16-byte A copies / 128 threads
       const int e = threadIdx.x + MM_THREADS * i;
       if (!ADJ) {
         const int k = e >> 5, p = e & 31;  // column k, row pair p
         const bool ok = 2 * p < tl.count && kb + k < kend;
         cp_async<16>(dA + k * RB_AP + 2 * p, ok ? T + (int64_t)(kb + k) * ld + tl.start + 2 * p : T, ok);
       } else {
-        const int m = e >> 4, p = e & 15;  // tile row m (T column), k pair p
+        const int m = e / (RB_BK / 2), p = e % (RB_BK / 2);  // tile row m (T column), k pair p
         const bool ok = m < tl.count && kb + 2 * p < kend;
         cp_async<16>(dA + m * RB_KP + 2 * p, ok ? T + (int64_t)(tl.start + m) * ld + kb + 2 * p : T, ok);
       }
     }
-    S *drow = Bs + (kc & 1) * B_CH + brow * RB_NP + 8 * bq;
+    S *drow = Bs + (kc % NSTG) * B_CH + brow * RB_NP + RPT * bq;
     const S *srow = nullptr;
     bool contiguous = false;
     int64_t rstride = 0;
@@ -1360,21 +1393,21 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_real_kernel(const Ctx cx, c
     }
     if (reg_path) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int n = 8 * bq + j;
+      for (int j = 0; j < RPT; ++j) {
+        const int n = RPT * bq + j;
         const bool ok = qr >= 0 && n < nv;
         drow[j] = ok ? (ADJ ? (contiguous ? srow[n] : srow[n * rstride]) : in_value<S>(cx, B, qr, rhs0 + n)) : 0.0;
       }
     } else if (contiguous && even) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int n = 8 * bq + 2 * j;
+      for (int j = 0; j < RPT / 2; ++j) {
+        const int n = RPT * bq + 2 * j;
         cp_async<16>(drow + 2 * j, srow + n, qr >= 0 && n < nv);
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int n = 8 * bq + j;
+      for (int j = 0; j < RPT; ++j) {
+        const int n = RPT * bq + j;
         const bool ok = qr >= 0 && n < nv;
         cp_async<8>(drow + j, ok ? (contiguous ? srow + n : srow + n * rstride) : static_cast<const S *>(cx.z), ok);
       }
@@ -1389,24 +1422,27 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_real_kernel(const Ctx cx, c
 #pragma unroll
   for (int v = 0; v < 4; ++v) c2[0][v] = 0.0;
 
+  // NSTG-stage ring: chunks kc+1 .. kc+NSTG-1 in flight while chunk kc computes
   int qn = nchunks > 0 ? row_index(0) : -1;
-  if (nchunks > 0) {
-    load(0, qn);
-    cp_async_commit();
-    if (nchunks > 1) qn = row_index(1);
-    cp_async_wait<0>();
-    __syncthreads();
+#pragma unroll
+  for (int st = 0; st < NSTG - 1; ++st) {
+    if (st < nchunks) {
+      load(st, qn);
+      if (st + 1 < nchunks) qn = row_index(st + 1);
+    }
+    cp_async_commit();  // (empty groups keep the group count uniform)
   }
   const int m0 = warp * 16 + gid;
   for (int kc = 0; kc < nchunks; ++kc) {
-    const bool more = kc + 1 < nchunks;
-    if (more) {
-      load(kc + 1, qn);
-      cp_async_commit();
-      if (kc + 2 < nchunks) qn = row_index(kc + 2);
+    cp_async_wait<NSTG - 2>();  // chunk kc has landed (this thread's copies)
+    __syncthreads();            // ... everyone's; and chunk kc-1's buffer is free
+    if (kc + NSTG - 1 < nchunks) {
+      load(kc + NSTG - 1, qn);
+      if (kc + NSTG < nchunks) qn = row_index(kc + NSTG);
     }
-    const S *Ac = As + (kc & 1) * A_CH;
-    const S *Bc = Bs + (kc & 1) * B_CH;
+    cp_async_commit();
+    const S *Ac = As + (kc % NSTG) * A_CH;
+    const S *Bc = Bs + (kc % NSTG) * B_CH;
 #pragma unroll
     for (int k4 = 0; k4 < KS; ++k4) {
       const int k = 4 * k4 + tig;
@@ -1415,9 +1451,9 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_real_kernel(const Ctx cx, c
 #pragma unroll
       for (int t = 0; t < NT; ++t) dmma(c0[t], a0, a1, Bc[k * RB_NP + 8 * t + gid]);
     }
-    cp_async_wait<0>();
-    __syncthreads();
   }
+  cp_async_wait<0>();
+  __syncthreads();  // operand buffers free (the K-split flag reuses them)
   mma_epilogue<S, ADJ, NT, false, 0>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
 }
 
@@ -1428,15 +1464,33 @@ inline bool mma_real16() {
   return !(e && atoi(e) == 0);
 }
 
-template <bool ADJ>
-void mma_real_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
-  constexpr int smem = rb_smem_bytes<ADJ>();
+// pipeline variant: MHT_REAL_CFG = 0 (K chunk 32, 2 stages) | 1 (32, 3) |
+// 2 (16, 3; default: c3 forward 6.9 -> 6.1 ms, adjoint 7.7 -> 7.3 ms,
+// profiles/r01_real_cfg_ab.txt) | 3 (16, 4)
+inline int real_cfg() {
+  const char *e = getenv("MHT_REAL_CFG");
+  return e ? atoi(e) : 2;
+}
+
+template <bool ADJ, int BKT, int NSTG>
+void mma_real_launch_t(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
+  constexpr int smem = rb_smem_bytes<ADJ, BKT, NSTG>();
   static bool attr = [] {
-    cudaFuncSetAttribute(mma_real_kernel<ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(mma_real_kernel<ADJ, BKT, NSTG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)attr;
-  mma_real_kernel<ADJ><<<dim3((cx.nrhs + 31) / 32, nt), MM_THREADS, smem, st>>>(cx, tiles, from_f);
+  mma_real_kernel<ADJ, BKT, NSTG><<<dim3((cx.nrhs + 31) / 32, nt), MM_THREADS, smem, st>>>(cx, tiles, from_f);
+}
+
+template <bool ADJ>
+void mma_real_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
+  switch (real_cfg()) {
+    case 1: mma_real_launch_t<ADJ, 32, 3>(cx, tiles, nt, from_f, st); break;
+    case 3: mma_real_launch_t<ADJ, 16, 4>(cx, tiles, nt, from_f, st); break;
+    case 0: mma_real_launch_t<ADJ, 32, 2>(cx, tiles, nt, from_f, st); break;
+    default: mma_real_launch_t<ADJ, 16, 3>(cx, tiles, nt, from_f, st);
+  }
 }
 
 // Multi-RHS configuration (compile-time variants; default picked from the

@@ -688,14 +688,15 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
     if (!maps.empty())
       CUDA_TRY(cudaMemcpy(P->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     P->device_bytes += (int64_t)maps.size() * (int64_t)sizeof(CUtensorMap);
-    // real forward tiles: box = 16 rows (128 B) x BK columns, 128-byte swizzle
-    if (!P->cplx) {
+    // forward tiles: box = 128-byte rows (16 real / 8 complex) x BK columns,
+    // 128-byte swizzle
+    {
       std::vector<CUtensorMap> fmaps(blocks.size());
       for (size_t i = 0; i < blocks.size(); ++i) {
         const DevBlock &D = blocks[i];
         memset(&fmaps[i], 0, sizeof(CUtensorMap));
         if (D.n_red == 0 || D.r_out == 0) continue;
-        cuuint64_t dims[2] = {(cuuint64_t)D.r_out, (cuuint64_t)D.n_red};
+        cuuint64_t dims[2] = {(cuuint64_t)D.r_out * ew, (cuuint64_t)D.n_red};
         cuuint64_t strides[1] = {(cuuint64_t)D.ld * P->ssz};
         cuuint32_t box[2] = {16, (cuuint32_t)bk};
         cuuint32_t estr[2] = {1, 1};
