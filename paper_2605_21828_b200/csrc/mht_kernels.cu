@@ -1111,31 +1111,49 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
           }
         }
       } else {
+        // a lane's KS rows: base pointer and right-hand-side stride resolved
+        // once per row (segment / source / perm), then one multiply-add per element
+        const S *rb[KS];
+        int64_t rs[KS];
 #pragma unroll
-      for (int i = 0; i < B_CH / 32; ++i) {
-        const int k4 = i / NT, t = i % NT;
-        const int r = rhs0 + t * 8 + gid_;
-        const int qq = q[k4];
-        const bool ok = qq >= 0 && r < cx.nrhs;
-        const S *src = static_cast<const S *>(cx.z);  // any valid address when !ok (zero fill)
-        if (ok) {
-          if (ADJ) {
-            src = from_f_ ? static_cast<const S *>(cx.fin) + (int64_t)r * cx.n + qq
-                          : static_cast<const S *>(cx.z) + (B.out_off + qq) * cx.nrhs + r;
-          } else {
-            const bool s1 = qq >= B.seg_len[0];
-            const int64_t off = s1 ? B.seg_off[1] + (qq - B.seg_len[0]) : B.seg_off[0] + qq;
-            const int32_t srcsel = s1 ? B.seg_src[1] : B.seg_src[0];
-            src = srcsel == SRC_C ? static_cast<const S *>(cx.c) + (int64_t)r * cx.m + off
-                                  : static_cast<const S *>(cx.z) + off * cx.nrhs + r;
+        for (int k4 = 0; k4 < KS; ++k4) {
+          const int qq = q[k4];
+          rb[k4] = static_cast<const S *>(cx.z);
+          rs[k4] = 0;
+          if (qq >= 0) {
+            if (ADJ) {
+              if (from_f_) {
+                rb[k4] = static_cast<const S *>(cx.fin) + qq;
+                rs[k4] = cx.n;
+              } else {
+                rb[k4] = static_cast<const S *>(cx.z) + (B.out_off + qq) * cx.nrhs;
+                rs[k4] = 1;
+              }
+            } else {
+              const bool s1 = qq >= B.seg_len[0];
+              const int64_t off = s1 ? B.seg_off[1] + (qq - B.seg_len[0]) : B.seg_off[0] + qq;
+              if ((s1 ? B.seg_src[1] : B.seg_src[0]) == SRC_C) {
+                rb[k4] = static_cast<const S *>(cx.c) + off;
+                rs[k4] = cx.m;
+              } else {
+                rb[k4] = static_cast<const S *>(cx.z) + off * cx.nrhs;
+                rs[k4] = 1;
+              }
+            }
           }
         }
-        if (!reg_path) {
-          cp_async<sizeof(S)>(dB + lane + 32 * i, src, ok);
-        } else {
-          dB[lane + 32 * i] = ok ? (ADJ ? *src : in_value<S>(cx, B, qq, r)) : X::zero();
+#pragma unroll
+        for (int i = 0; i < B_CH / 32; ++i) {
+          const int k4 = i / NT, t = i % NT;
+          const int r = rhs0 + t * 8 + gid_;
+          const bool ok = q[k4] >= 0 && r < cx.nrhs;
+          const S *src = ok ? rb[k4] + (int64_t)r * rs[k4] : static_cast<const S *>(cx.z);
+          if (!reg_path) {
+            cp_async<sizeof(S)>(dB + lane + 32 * i, src, ok);
+          } else {
+            dB[lane + 32 * i] = ok ? (ADJ ? *src : in_value<S>(cx, B, q[k4], r)) : X::zero();
+          }
         }
-      }
       }
       mbar_cp_async_arrive(full + slot);  // completes when this lane's cp.async have landed
       mbar_arrive(full + slot);           // the register-path stores (if any) are done
