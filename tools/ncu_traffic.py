@@ -29,9 +29,10 @@ def phase_of(name: str, width: int) -> str | None:
         return "fwd@1"
     if name.startswith("adj_kernel"):
         return "adj@1"
-    if name.startswith("mma_kernel") or name.startswith("mma_ws_kernel"):
+    if name.startswith("mma_kernel") or name.startswith("mma_ws_kernel") or name.startswith("mma_real_kernel"):
         args = name[name.index("<") + 1:].split(",")
-        adj = args[1].strip() in ("1", "true")
+        flag = args[0] if name.startswith("mma_real_kernel") else args[1]  # mma_real_kernel<ADJ, ...>
+        adj = flag.strip().rstrip(">") in ("1", "true")
         return f"{'adj' if adj else 'fwd'}@{width}"
     if name.startswith("reduce_kernel"):
         return "sum"
