@@ -331,7 +331,7 @@ __device__ __forceinline__ S adj_in(const Ctx &cx, const DevBlock &B, int i, int
 // partial column sums to scratch and the last CTA of the group to arrive adds
 // them in split order (deterministic, no float atomics).
 // ------------------------------------------------------------------------
-template <class S, int RB, bool CG, int RCH = ADJ_RCH>
+template <class S, int RB, bool CG, int RCH = ADJ_RCH, bool AR2 = false>
 __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_f, int rhs0) {
   using X = Tr<S>;
   // columns per warp: 8 complex / 16 real
@@ -391,17 +391,38 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
         }
       }
     } else if (cbase < cend) {
-      for (int i = lane; i < rn; i += 32) {
-        S zv[RB];
+      if constexpr (AR2) {
+        // two rows per lane per step (i, i + 32): 2 CPW 16-byte loads in flight
+        for (int i = lane; i < rn; i += 64) {
+          const bool v2 = i + 32 < rn;
+          const S z0 = zs[i][0], z1 = v2 ? zs[i + 32][0] : X::zero();
+          S t0[CPW], t1[CPW];
 #pragma unroll
-        for (int k = 0; k < RB; ++k) zv[k] = zs[i][k];
-        S t[CPW];
+          for (int u = 0; u < CPW; ++u) {
+            const bool cu = cbase + u < cend;
+            const S *cp = T + (int64_t)(cbase + u) * ld + rc + i;
+            t0[u] = cu ? X::ldT(cp) : X::zero();
+            t1[u] = (cu && v2) ? X::ldT(cp + 32) : X::zero();
+          }
 #pragma unroll
-        for (int u = 0; u < CPW; ++u) t[u] = cbase + u < cend ? X::ldT(T + (int64_t)(cbase + u) * ld + rc + i) : X::zero();
+          for (int u = 0; u < CPW; ++u) {
+            X::fmac(acc[u][0], t0[u], z0);
+            X::fmac(acc[u][0], t1[u], z1);
+          }
+        }
+      } else {
+        for (int i = lane; i < rn; i += 32) {
+          S zv[RB];
 #pragma unroll
-        for (int u = 0; u < CPW; ++u)
+          for (int k = 0; k < RB; ++k) zv[k] = zs[i][k];
+          S t[CPW];
 #pragma unroll
-          for (int k = 0; k < RB; ++k) X::fmac(acc[u][k], t[u], zv[k]);
+          for (int u = 0; u < CPW; ++u) t[u] = cbase + u < cend ? X::ldT(T + (int64_t)(cbase + u) * ld + rc + i) : X::zero();
+#pragma unroll
+          for (int u = 0; u < CPW; ++u)
+#pragma unroll
+            for (int k = 0; k < RB; ++k) X::fmac(acc[u][k], t[u], zv[k]);
+        }
       }
     }
     __syncthreads();
@@ -462,7 +483,7 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
   }
 }
 
-template <class S, int RB, int RCH = ADJ_RCH>
+template <class S, int RB, int RCH = ADJ_RCH, bool AR2 = false>
 __global__ void __launch_bounds__(ADJ_THREADS, 7) adj_kernel(const Ctx cx, const Tile *__restrict__ tiles,
                                                              int from_f) {
   const Tile tl = tiles[blockIdx.y];
@@ -481,7 +502,13 @@ __global__ void __launch_bounds__(ADJ_THREADS, 7) adj_kernel(const Ctx cx, const
     }
   }
   pdl_wait();
-  adj_tile<S, RB, false, RCH>(cx, tl, from_f, blockIdx.x * RB);
+  adj_tile<S, RB, false, RCH, AR2>(cx, tl, from_f, blockIdx.x * RB);
+}
+
+// complex adjoint, two rows per lane per step (MHT_ADJ_AR2=1, experiment)
+inline bool adj_ar2() {
+  const char *e = getenv("MHT_ADJ_AR2");
+  return e && atoi(e) == 1;
 }
 
 // rows of z staged per pass: MHT_ADJ_RCH=512|1024 (experiments), default ADJ_RCH
@@ -1688,6 +1715,8 @@ void adj_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cuda
       launch_pdl(adj_kernel<S, 1, 256>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
     else if (adj_rch() == 512)
       launch_pdl(adj_kernel<S, 1, 512>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
+    else if (sizeof(S) == 16 && adj_ar2())
+      launch_pdl(adj_kernel<S, 1, ADJ_RCH, true>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
     else
       launch_pdl(adj_kernel<S, 1>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
   }
