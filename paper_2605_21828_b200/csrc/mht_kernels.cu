@@ -505,10 +505,11 @@ __global__ void __launch_bounds__(ADJ_THREADS, 7) adj_kernel(const Ctx cx, const
   adj_tile<S, RB, false, RCH, AR2>(cx, tl, from_f, blockIdx.x * RB);
 }
 
-// complex adjoint, two rows per lane per step (MHT_ADJ_AR2=1, experiment)
+// complex adjoint, two rows per lane per step (default; MHT_ADJ_AR2=0: one):
+// c2 adj_nrhs1 6.60 -> 6.56 ms (profiles/r01_adj_ar2_ab.txt)
 inline bool adj_ar2() {
   const char *e = getenv("MHT_ADJ_AR2");
-  return e && atoi(e) == 1;
+  return !(e && atoi(e) == 0);
 }
 
 // rows of z staged per pass: MHT_ADJ_RCH=512|1024 (experiments), default ADJ_RCH
