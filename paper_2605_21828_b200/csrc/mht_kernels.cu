@@ -622,37 +622,75 @@ __device__ __forceinline__ void mma_epilogue(const Ctx &cx, const Tile &tl, cons
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const bool red_iota = (B.flags & F_RED_IOTA) != 0;
+  // a thread's fragments cover two tile rows (h = 0: gid, 1: gid + 8).  Every
+  // index and skeleton load is issued before the first store: the stores
+  // could alias the loaded arrays as far as the compiler knows, so
+  // interleaving them serialised 2 + 4 NT dependent global round trips per
+  // thread (c3 stage 3: 15 us per CTA, long_scoreboard 57%,
+  // profiles/r01_epilogue_hoist_ab.txt)
+  int mh[2], qh[2];
+  bool okh[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    mh[h] = warp * 16 + tile_row<S, MODE>(gid + 8 * h);
+    okh[h] = mh[h] < tl.count;
+    const int row = tl.start + mh[h];
+    if (!ADJ) {
+      qh[h] = (okh[h] && row < B.n_skel) ? ((B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row]) : -1;
+    } else if (ksplit) {
+      qh[h] = 0;
+    } else {
+      qh[h] = okh[h] ? (red_iota ? row : cx.idx[B.red_off + row]) : 0;
+    }
+  }
+  int oh[2] = {0, 0};  // forward leaf stage: output rows through perm_x
+  if (!ADJ && (B.flags & F_OUT_F)) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) oh[h] = okh[h] ? cx.perm[B.out_off + tl.start + mh[h]] : 0;
+  }
+  // accumulators -> values first (the 3M form's three planes collapse to
+  // one), so the skeleton loads below do not hold all of them live
+  S val[NT][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      if constexpr (!CPLX) {
+        val[t][v] = c0[t][v];
+      } else if constexpr (G3) {
+        val[t][v] = make_double2(c0[t][v] - c1[t][v], c2[t][v] - c0[t][v] - c1[t][v]);
+      } else {
+        val[t][v] = make_double2(c0[t][v], c1[t][v]);
+      }
+    }
+  if (!ADJ) {  // forward: out = T in[red] + in[skel]
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int r = rhs0 + t * 8 + 2 * tig + (v & 1);
+        if (qh[v >> 1] >= 0 && r < cx.nrhs) val[t][v] = X::add(val[t][v], in_value<S>(cx, B, qh[v >> 1], r));
+      }
+  }
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const int m = warp * 16 + tile_row<S, MODE>(gid + 8 * (v >> 1));
+      const int h = v >> 1;
+      const int m = mh[h];
       const int r = rhs0 + t * 8 + 2 * tig + (v & 1);
-      if (m >= tl.count || r >= cx.nrhs) continue;
-      S val;
-      if constexpr (!CPLX) {
-        val = c0[t][v];
-      } else if constexpr (G3) {
-        val = make_double2(c0[t][v] - c1[t][v], c2[t][v] - c0[t][v] - c1[t][v]);
-      } else {
-        val = make_double2(c0[t][v], c1[t][v]);
-      }
+      if (!okh[h] || r >= cx.nrhs) continue;
       const int row = tl.start + m;
       if (!ADJ) {
-        if (row < B.n_skel) {
-          const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
-          val = X::add(val, in_value<S>(cx, B, q, r));
-        }
         if (B.flags & F_OUT_F)
-          static_cast<S *>(cx.fout)[r * cx.n + cx.perm[B.out_off + row]] = val;
+          static_cast<S *>(cx.fout)[r * cx.n + oh[h]] = val[t][v];
         else
-          static_cast<S *>(cx.z)[(B.out_off + row) * cx.nrhs + r] = val;
+          static_cast<S *>(cx.z)[(B.out_off + row) * cx.nrhs + r] = val[t][v];
       } else if (ksplit) {
         const int64_t slab = B.msp_off + (int64_t)(tl.start / MMA_COLS) * B.mks + sidx;
-        static_cast<S *>(cx.msplit)[(slab * MMA_COLS + m) * cx.nrhs + r] = val;
+        static_cast<S *>(cx.msplit)[(slab * MMA_COLS + m) * cx.nrhs + r] = val[t][v];
       } else {
-        const int q = red_iota ? row : cx.idx[B.red_off + row];
-        static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = val;
+        static_cast<S *>(cx.part)[(B.part_off + qh[h]) * cx.nrhs + r] = val[t][v];
       }
     }
   }
@@ -664,11 +702,28 @@ __device__ __forceinline__ void mma_epilogue(const Ctx &cx, const Tile &tl, cons
     const int chunk = (B.n_skel + ntl - 1) / ntl;
     const int i0 = (tl.start / MMA_COLS) * chunk, i1 = min(B.n_skel, i0 + chunk);
     const int ni = i1 - i0;
-    for (int e = threadIdx.x; e < ni * NRT; e += MM_THREADS) {
-      const int i = i0 + e / NRT, r = rhs0 + e % NRT;  // RHS fastest: contiguous 32-wide rows
-      if (r >= cx.nrhs) continue;
-      const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
-      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + r] = adj_in<S>(cx, B, i, r, from_f != 0);
+    // batches of SKB copies per thread, loads before stores (as above)
+    constexpr int SKB = 4;
+    for (int e0 = threadIdx.x; e0 < ni * NRT; e0 += SKB * MM_THREADS) {
+      S v[SKB];
+      int q[SKB];
+#pragma unroll
+      for (int u = 0; u < SKB; ++u) {
+        const int e = e0 + u * MM_THREADS;
+        const int i = i0 + e / NRT, r = rhs0 + e % NRT;  // RHS fastest: contiguous 32-wide rows
+        const bool ok = e < ni * NRT && r < cx.nrhs;
+        q[u] = !ok ? -1 : ((B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i]);
+      }
+#pragma unroll
+      for (int u = 0; u < SKB; ++u) {
+        const int e = e0 + u * MM_THREADS;
+        v[u] = q[u] >= 0 ? adj_in<S>(cx, B, i0 + e / NRT, rhs0 + e % NRT, from_f != 0) : X::zero();
+      }
+#pragma unroll
+      for (int u = 0; u < SKB; ++u) {
+        const int e = e0 + u * MM_THREADS;
+        if (q[u] >= 0) static_cast<S *>(cx.part)[(B.part_off + q[u]) * cx.nrhs + rhs0 + e % NRT] = v[u];
+      }
     }
   }
   if (ADJ && ksplit) {
