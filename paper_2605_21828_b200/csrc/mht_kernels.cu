@@ -34,6 +34,32 @@ constexpr unsigned FULL = 0xffffffffu;
 // a launch without the PDL attribute.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// launch with the programmatic-stream-serialisation attribute (PDL) unless
+// MHT_PDL=0; read per launch (graphs capture the attribute as a programmatic
+// edge).  Every kernel launched this way calls pdl_wait() before its first
+// access to memory an earlier kernel of the sequence writes or reads.
+inline bool pdl_on() {
+  const char *e = getenv("MHT_PDL");
+  return !(e && atoi(e) == 0);
+}
+template <class... KArgs, class... Args>
+void launch_pdl_smem(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  launch_pdl_smem(kern, grid, block, 0, st, args...);
+}
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 template <class S>
@@ -773,7 +799,8 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
   __shared__ __align__(16) S As[NB * A_CH];
   __shared__ __align__(16) S Bs[NB * B_CH];
 
-  const Tile tl = tiles[blockIdx.y];
+  pdl_trigger();
+  const Tile tl = tiles[blockIdx.y];  // plan tables: never written by kernels
   const DevBlock B = cx.blocks[tl.blk];
   const int rhs0 = blockIdx.x * NRT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -854,10 +881,13 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_kernel(const Ctx cx, con
 #pragma unroll
     for (int v = 0; v < 4; ++v) c2[t][v] = 0.0;
 
-  // two-stage ring, sync at the bottom of the iteration
+  if (nchunks == 0) pdl_wait();
+  // two-stage ring, sync at the bottom of the iteration.  The first factor
+  // chunk does not depend on earlier kernels: it streams in before pdl_wait()
   if (nchunks > 0) {
     load_A(0);
     cp_async_commit();
+    pdl_wait();  // the previous stage's workspace is complete and visible
     load_q(0);
     load_B(0);
     store_B(0);
@@ -1027,7 +1057,8 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   uint64_t *full = reinterpret_cast<uint64_t *>(Bs + NS * B_CH);
   uint64_t *empty = full + NS;
 
-  const Tile tl = tiles[blockIdx.y];
+  pdl_trigger();
+  const Tile tl = tiles[blockIdx.y];  // plan tables: never written by kernels
   const DevBlock B = cx.blocks[tl.blk];
   const int rhs0 = blockIdx.x * NRT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1057,6 +1088,7 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();  // the previous stage's workspace is complete and visible
 
   if (warp == AW) {
     // ------------------------------------------------ producer warp
@@ -1359,7 +1391,8 @@ void mma_ws_launch_t(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaS
     return true;
   }();
   (void)attr;
-  mma_ws_kernel<S, ADJ, M3, MINB, FM><<<dim3((cx.nrhs + 31) / 32, nt), WS_THREADS, smem, st>>>(cx, tiles, from_f);
+  launch_pdl_smem(mma_ws_kernel<S, ADJ, M3, MINB, FM>, dim3((cx.nrhs + 31) / 32, nt), dim3(WS_THREADS), smem, st, cx, tiles,
+                  from_f);
 }
 
 // complex forward A tile: MHT_WS_FMODE=3 (2-D TMA, swizzled) | 0 (1-D bulk
@@ -1419,7 +1452,8 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_real_kernel(const Ctx cx, c
   S *As = reinterpret_cast<S *>(rb_smem);
   S *Bs = As + NSTG * A_CH;
 
-  const Tile tl = tiles[blockIdx.y];
+  pdl_trigger();
+  const Tile tl = tiles[blockIdx.y];  // plan tables: never written by kernels
   const DevBlock B = cx.blocks[tl.blk];
   const int rhs0 = blockIdx.x * 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1515,6 +1549,7 @@ __global__ void __launch_bounds__(MM_THREADS, 4) mma_real_kernel(const Ctx cx, c
     }
   };
 
+  pdl_wait();  // the previous stage's workspace is complete and visible
   double c0[NT][4], c1[NT][4], c2[1][4];
 #pragma unroll
   for (int t = 0; t < NT; ++t)
@@ -1581,7 +1616,8 @@ void mma_real_launch_t(const Ctx &cx, const Tile *tiles, int nt, int from_f, cud
     return true;
   }();
   (void)attr;
-  mma_real_kernel<ADJ, BKT, NSTG><<<dim3((cx.nrhs + 31) / 32, nt), MM_THREADS, smem, st>>>(cx, tiles, from_f);
+  launch_pdl_smem(mma_real_kernel<ADJ, BKT, NSTG>, dim3((cx.nrhs + 31) / 32, nt), dim3(MM_THREADS), smem, st, cx, tiles,
+                  from_f);
 }
 
 template <bool ADJ>
@@ -1608,7 +1644,8 @@ inline int mma_variant() {
 
 template <class S, bool ADJ, int NT, bool M3, int MINB>
 void mma_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
-  mma_kernel<S, ADJ, NT, M3, MINB><<<dim3((cx.nrhs + 8 * NT - 1) / (8 * NT), nt), MM_THREADS, 0, st>>>(cx, tiles, from_f);
+  launch_pdl(mma_kernel<S, ADJ, NT, M3, MINB>, dim3((cx.nrhs + 8 * NT - 1) / (8 * NT), nt), dim3(MM_THREADS), st, cx, tiles,
+             from_f);
 }
 
 template <class S, bool ADJ, bool M3, int MINB, int NTMAX>
@@ -1673,27 +1710,6 @@ __global__ void __launch_bounds__(256) reduce_kernel(const Ctx cx, const Piece *
   reduce_piece<S, false>(cx, pieces[blockIdx.x], rd, blockIdx.y, gridDim.y);  // y: slices of wide pieces
 }
 
-// launch with the programmatic-stream-serialisation attribute (PDL) unless
-// MHT_PDL=0; read per launch (graphs capture the attribute as a programmatic
-// edge)
-inline bool pdl_on() {
-  const char *e = getenv("MHT_PDL");
-  return !(e && atoi(e) == 0);
-}
-template <class... KArgs, class... Args>
-void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_on() ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, args...);
-}
 
 // ------------------------------------------------------------------------
 // persistent nrhs = 1 apply: ONE cooperative launch walks all phases of a
