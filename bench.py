@@ -418,8 +418,9 @@ def main():
                 "frac": achieved / peaks["dmma_tflops"],
                 "frac_of_nominal": achieved / (148 * 64 * 2 * 1.965e9 / 1e12),  # 37.2 TF: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz
                 "traffic": traffic, "algorithmic_flops_per_launch": alg,
-                "kernel": (f"{'mma_ws_kernel' if P.is_complex else 'mma_kernel'} {dkind} nrhs={dr} "
-                           f"(DMMA m16n8k4 f64{', TMA + warp-specialised' if P.is_complex else ''})"),
+                "kernel": (f"{'mma_ws_kernel' if P.is_complex else 'mma_real_kernel'} {dkind} nrhs={dr} "
+                           f"(DMMA m16n8k4 f64, "
+                           f"{'TMA + warp-specialised' if P.is_complex else 'cp.async ring, 6 CTAs/SM'})"),
                 "peak_source": peaks["dmma_src"]}
         if P.is_complex:
             roof["note"] = ("achieved counts 8 real flops per complex multiply-add (algorithmic); the kernel "

@@ -1438,8 +1438,8 @@ __host__ __device__ constexpr int rb_smem_bytes() {
   return NSTG * (rb_a_elems<ADJ, BKT>() + BKT * RB_NP) * 8;
 }
 
-template <bool ADJ, int BKT, int NSTG>
-__global__ void __launch_bounds__(MM_THREADS, 4) mma_real_kernel(const Ctx cx, const Tile *__restrict__ tiles,
+template <bool ADJ, int BKT, int NSTG, int MINB = 4>
+__global__ void __launch_bounds__(MM_THREADS, MINB) mma_real_kernel(const Ctx cx, const Tile *__restrict__ tiles,
                                                                   int from_f) {
   using S = double;
   using X = Tr<S>;
@@ -1600,23 +1600,26 @@ inline bool mma_real16() {
   return !(e && atoi(e) == 0);
 }
 
-// pipeline variant: MHT_REAL_CFG = 0 (K chunk 32, 2 stages) | 1 (32, 3) |
-// 2 (16, 3; default: c3 forward 6.9 -> 6.1 ms, adjoint 7.7 -> 7.3 ms,
-// profiles/r01_real_cfg_ab.txt) | 3 (16, 4)
+// pipeline variant: MHT_REAL_CFG = 0 (K chunk 32, 2 stages, 4 CTAs/SM) |
+// 1 (32, 3) | 2 (16, 3; c3 forward 6.9 -> 6.1 ms, adjoint 7.7 -> 7.3 ms over 0,
+// profiles/r01_real_cfg_ab.txt) | 3 (16, 4) | 4 (16, 3, 5 CTAs/SM) |
+// 5 (16, 2, 6 CTAs/SM, 80 registers; default: c3 +1.5% over 2 in four
+// back-to-back pairs, profiles/r01_real_occupancy_ab.txt) | 6 (16, 2, 7) |
+// 7 (8, 4, 6)
 inline int real_cfg() {
   const char *e = getenv("MHT_REAL_CFG");
-  return e ? atoi(e) : 2;
+  return e ? atoi(e) : 5;
 }
 
-template <bool ADJ, int BKT, int NSTG>
+template <bool ADJ, int BKT, int NSTG, int MINB = 4>
 void mma_real_launch_t(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
   constexpr int smem = rb_smem_bytes<ADJ, BKT, NSTG>();
   static bool attr = [] {
-    cudaFuncSetAttribute(mma_real_kernel<ADJ, BKT, NSTG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(mma_real_kernel<ADJ, BKT, NSTG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)attr;
-  launch_pdl_smem(mma_real_kernel<ADJ, BKT, NSTG>, dim3((cx.nrhs + 31) / 32, nt), dim3(MM_THREADS), smem, st, cx, tiles,
+  launch_pdl_smem(mma_real_kernel<ADJ, BKT, NSTG, MINB>, dim3((cx.nrhs + 31) / 32, nt), dim3(MM_THREADS), smem, st, cx, tiles,
                   from_f);
 }
 
@@ -1626,7 +1629,11 @@ void mma_real_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaS
     case 1: mma_real_launch_t<ADJ, 32, 3>(cx, tiles, nt, from_f, st); break;
     case 3: mma_real_launch_t<ADJ, 16, 4>(cx, tiles, nt, from_f, st); break;
     case 0: mma_real_launch_t<ADJ, 32, 2>(cx, tiles, nt, from_f, st); break;
-    default: mma_real_launch_t<ADJ, 16, 3>(cx, tiles, nt, from_f, st);
+    case 4: mma_real_launch_t<ADJ, 16, 3, 5>(cx, tiles, nt, from_f, st); break;
+    case 6: mma_real_launch_t<ADJ, 16, 2, 7>(cx, tiles, nt, from_f, st); break;
+    case 7: mma_real_launch_t<ADJ, 8, 4, 6>(cx, tiles, nt, from_f, st); break;
+    case 2: mma_real_launch_t<ADJ, 16, 3>(cx, tiles, nt, from_f, st); break;
+    default: mma_real_launch_t<ADJ, 16, 2, 6>(cx, tiles, nt, from_f, st);
   }
 }
 
