@@ -398,7 +398,31 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
       // real: lane takes the row pair (2q, 2q + 1) of each of its columns with
       // one 16-byte load (rc is even; the pad row of an odd r_out is zero)
       static_assert(!REAL || RB == 1, "real pair path is the nrhs = 1 kernel");
-      if (cbase < cend) {
+      if (cbase < cend && AR2) {
+        // two row pairs per lane per step (2q, 2q + 1 and 2q + 64, 2q + 65):
+        // 2 CPW 16-byte loads in flight
+        for (int q = lane; 2 * q < rn; q += 64) {
+          const bool v2 = 2 * (q + 32) < rn;
+          const double z0 = zs[2 * q][0], z1 = zs[2 * q + 1][0];
+          const double z2 = v2 ? zs[2 * q + 64][0] : 0.0, z3 = v2 ? zs[2 * q + 65][0] : 0.0;
+          double2 t0[CPW], t1[CPW];
+#pragma unroll
+          for (int u = 0; u < CPW; ++u) {
+            const bool cu = cbase + u < cend;
+            const double *cp = reinterpret_cast<const double *>(T) + (int64_t)(cbase + u) * ld + rc + 2 * q;
+            t0[u] = cu ? Tr<double>::ldT2(cp) : make_double2(0.0, 0.0);
+            t1[u] = (cu && v2) ? Tr<double>::ldT2(cp + 64) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < CPW; ++u) {
+            double &a = reinterpret_cast<double &>(acc[u][0]);
+            a = ::fma(t0[u].x, z0, a);
+            a = ::fma(t0[u].y, z1, a);
+            a = ::fma(t1[u].x, z2, a);
+            a = ::fma(t1[u].y, z3, a);
+          }
+        }
+      } else if (cbase < cend) {
         for (int q = lane; 2 * q < rn; q += 32) {
           const double z0 = zs[2 * q][0], z1 = zs[2 * q + 1][0];
           // all CPW column loads issued before their first use (predicated)
@@ -539,6 +563,11 @@ inline bool adj_ar2() {
 }
 
 // rows of z staged per pass: MHT_ADJ_RCH=512|1024 (experiments), default ADJ_RCH
+// real adjoint, two row pairs per lane per step: MHT_ADJ_AR2R=1
+inline bool adj_ar2_real() {
+  const char *e = getenv("MHT_ADJ_AR2R");
+  return e && atoi(e) == 1;
+}
 inline int adj_rch() {
   static int v = [] {
     const char *e = getenv("MHT_ADJ_RCH");
@@ -1794,7 +1823,7 @@ void adj_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cuda
       launch_pdl(adj_kernel<S, 1, 256>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
     else if (adj_rch() == 512)
       launch_pdl(adj_kernel<S, 1, 512>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
-    else if (sizeof(S) == 16 && adj_ar2())
+    else if (sizeof(S) == 16 ? adj_ar2() : adj_ar2_real())
       launch_pdl(adj_kernel<S, 1, ADJ_RCH, true>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
     else
       launch_pdl(adj_kernel<S, 1>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
