@@ -488,3 +488,32 @@ def test_multi_rhs_kernels_repeatable(gpu, oracle_lib, plans, ws_mode, family):
         P.close()
     finally:
         os.environ.pop("MHT_MMA_WS", None)
+
+
+@pytest.mark.parametrize("real_cfg", ["0", "1", "2", "3", "4", "6", "7"])
+def test_real_kernel_variants(gpu, oracle_lib, plans, real_cfg):
+    """Every selectable real multi-RHS pipeline (MHT_REAL_CFG: K chunk 32/16/8,
+    2-4 stages, 4-7 CTAs/SM; the default 5 runs in every other test) matches
+    O2 at an even and an odd width, and the opt-in two-row-pair real nrhs = 1
+    adjoint (MHT_ADJ_AR2R=1) matches it too."""
+    os.environ["MHT_REAL_CFG"] = real_cfg
+    os.environ["MHT_ADJ_AR2R"] = "1"
+    try:
+        w = W.sphere_workload(4096, 63, 6, 1e-10)
+        path = str(plans / "sphere_rep.plan")
+        if not os.path.exists(path):
+            W.build_workload_plan(w, path, workers=8, log=None)
+        P = gpu.Plan(path)
+        P.set_graphs(False)
+        O = oracle_lib.Plan(path)
+        for nrhs in (1, 32, 33):
+            c = mi.real_gaussian(nrhs, w.m, 1200 + nrhs)
+            y = mi.real_gaussian(nrhs, w.n, 1300 + nrhs)
+            f = P.apply(torch.from_numpy(c).cuda()).cpu().numpy()
+            a = P.adjoint(torch.from_numpy(y).cuda()).cpu().numpy()
+            assert rel_cols(f, O.apply(c)) <= PARITY, ("fwd", real_cfg, nrhs)
+            assert rel_cols(a, O.adjoint(y)) <= PARITY, ("adj", real_cfg, nrhs)
+        P.close()
+    finally:
+        os.environ.pop("MHT_REAL_CFG", None)
+        os.environ.pop("MHT_ADJ_AR2R", None)
