@@ -42,8 +42,17 @@ inline bool pdl_on() {
   const char *e = getenv("MHT_PDL");
   return !(e && atoi(e) == 0);
 }
+// the multi-RHS kernels: PDL only with MHT_PDL_MMA=1 (neutral on c2 / c3,
+// 6% slower on c4's graph replay together with the 6-CTA real kernel,
+// profiles/r01_mma_pdl_ab.txt); their griddepcontrol instructions are no-ops
+// when launched without the attribute
+inline bool pdl_mma_on() {
+  const char *e = getenv("MHT_PDL_MMA");
+  return e && atoi(e) == 1 && pdl_on();
+}
 template <class... KArgs, class... Args>
-void launch_pdl_smem(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+void launch_ex(bool use_pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+               Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -53,12 +62,12 @@ void launch_pdl_smem(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_on() ? 1 : 0;
+  cfg.numAttrs = use_pdl ? 1 : 0;
   cudaLaunchKernelEx(&cfg, kern, args...);
 }
 template <class... KArgs, class... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
-  launch_pdl_smem(kern, grid, block, 0, st, args...);
+  launch_ex(pdl_on(), kern, grid, block, 0, st, args...);
 }
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
@@ -1420,8 +1429,8 @@ void mma_ws_launch_t(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaS
     return true;
   }();
   (void)attr;
-  launch_pdl_smem(mma_ws_kernel<S, ADJ, M3, MINB, FM>, dim3((cx.nrhs + 31) / 32, nt), dim3(WS_THREADS), smem, st, cx, tiles,
-                  from_f);
+  launch_ex(pdl_mma_on(), mma_ws_kernel<S, ADJ, M3, MINB, FM>, dim3((cx.nrhs + 31) / 32, nt), dim3(WS_THREADS), smem, st,
+            cx, tiles, from_f);
 }
 
 // complex forward A tile: MHT_WS_FMODE=3 (2-D TMA, swizzled) | 0 (1-D bulk
@@ -1648,8 +1657,8 @@ void mma_real_launch_t(const Ctx &cx, const Tile *tiles, int nt, int from_f, cud
     return true;
   }();
   (void)attr;
-  launch_pdl_smem(mma_real_kernel<ADJ, BKT, NSTG, MINB>, dim3((cx.nrhs + 31) / 32, nt), dim3(MM_THREADS), smem, st, cx, tiles,
-                  from_f);
+  launch_ex(pdl_mma_on(), mma_real_kernel<ADJ, BKT, NSTG, MINB>, dim3((cx.nrhs + 31) / 32, nt), dim3(MM_THREADS), smem,
+            st, cx, tiles, from_f);
 }
 
 template <bool ADJ>
@@ -1680,8 +1689,8 @@ inline int mma_variant() {
 
 template <class S, bool ADJ, int NT, bool M3, int MINB>
 void mma_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
-  launch_pdl(mma_kernel<S, ADJ, NT, M3, MINB>, dim3((cx.nrhs + 8 * NT - 1) / (8 * NT), nt), dim3(MM_THREADS), st, cx, tiles,
-             from_f);
+  launch_ex(pdl_mma_on(), mma_kernel<S, ADJ, NT, M3, MINB>, dim3((cx.nrhs + 8 * NT - 1) / (8 * NT), nt), dim3(MM_THREADS), 0,
+            st, cx, tiles, from_f);
 }
 
 template <class S, bool ADJ, bool M3, int MINB, int NTMAX>
