@@ -74,36 +74,55 @@ typedef struct {
 } mht_plan_info;
 
 /* Parse + validate a plan file, pack it into the level-contiguous device
- * layout and upload it to `device` (a CUDA ordinal).  Reads the whole file
+ * layout and upload it to `device` (a CUDA ordinal).  The plan holds the
+ * factorization of PAPER.md §2: space tree (perm_x, leaf
+ * offsets), frequency tree (leaf offsets), per-level ID transfer blocks
+ * X = [I T] Pi and the leaf interpolation blocks U_tau.  Reads the whole file
  * once; the checksum is verified on the fly.  *out is set only on MHT_OK.
  * Errors: MHT_ERR_IO (open/read), MHT_ERR_FORMAT (magic, version, checksum,
  * chain invariant r_in = r_out(p,c1) + r_out(p,c2)),
  * MHT_ERR_SHAPE, MHT_ERR_OOM, MHT_ERR_CUDA, MHT_ERR_UNSUPPORTED. */
 mht_status mht_plan_load(const char *path, int device, mht_plan **out);
 
+/* Sizes of the loaded plan (SPEC S:293-300 memory report: stored entries,
+ * bytes).  Never fails on a valid plan. */
 mht_status mht_plan_info_get(const mht_plan *plan, mht_plan_info *info);
 
 /* Stream for subsequent calls (a cudaStream_t passed as void*; NULL = the
  * legacy default stream).  Callers using PyTorch pass
- * torch.cuda.current_stream().cuda_stream. */
+ * torch.cuda.current_stream().cuda_stream.  The caller keeps ownership of
+ * `stream`; the plan's own loader stream stays owned by the plan.  Work
+ * queued on the previous stream is synchronised first. */
 mht_status mht_plan_set_stream(mht_plan *plan, void *stream);
 
 /* Pre-size the workspace for up to `nrhs` right-hand sides (otherwise grown
  * on demand by the first apply with a larger nrhs, which synchronises). */
 mht_status mht_reserve(mht_plan *plan, int nrhs);
 
-/* f = Phi_BF c.  c: device, m x nrhs (ld m); f: device, n x nrhs (ld n).
- * Runs leaf projection, the L transfer stages and the leaf interpolation
- * (with the perm_x scatter fused into the store). */
+/* Synthesis f = Phi_BF c (Eq. MHT-sum, f_j = sum_k c_k
+ * phi_k(x_j); evaluated through the factorization of §2, one
+ * multiply per stored factor).  c: device, m x nrhs (ld m), in
+ * the plan's frequency order; f: device, n x nrhs (ld n), user point order,
+ * fully overwritten.  Runs the leaf projection, the L transfer stages and the
+ * leaf interpolation (perm_x scatter fused into the store).  nrhs >= 1;
+ * c and f must not overlap.  Errors: MHT_ERR_INVALID_ARG (null, nrhs < 1,
+ * sharded plan), MHT_ERR_OOM (workspace growth), MHT_ERR_CUDA. */
 mht_status mht_apply(mht_plan *plan, const void *c, void *f, int nrhs);
 
-/* c = Phi_BF^* f.  f: device n x nrhs; c: device m x nrhs.  Exact reverse of
- * mht_apply with conjugate transposes; group sums are formed on load from
- * per-block partials (no atomics, bitwise deterministic). */
+/* Analysis c = Phi_BF^* f (the "fast adjoint transform", PAPER.md P:153-155,
+ * §1; used by the inverse MHT, and covariance products,
+ * P:1196-1198).  f: device n x nrhs (ld n, user point order); c: device
+ * m x nrhs (ld m), fully overwritten.  Exact reverse of mht_apply with
+ * conjugate transposes; the sum over the two transfers that read a block row
+ * is formed from per-block partials in a fixed order (no atomics, bitwise
+ * deterministic).  Errors as mht_apply. */
 mht_status mht_apply_adjoint(mht_plan *plan, const void *f, void *c, int nrhs);
 
-/* Same as above from/to HOST memory: copies c (or f) host->device on the plan
- * stream, applies, copies the result device->host and synchronises.  Host
+/* Same operations as mht_apply / mht_apply_adjoint from
+ * and to HOST memory: copies c (or f) host->device on the plan stream,
+ * applies, copies the result device->host and synchronises.  The output host
+ * buffer must hold n*nrhs (or m*nrhs) scalars of the plan's dtype (the C side
+ * cannot check this).  Host
  * buffers should be pinned for full copy bandwidth.  Used for the end-to-end
  * measurement. */
 mht_status mht_apply_host(mht_plan *plan, const void *c_host, void *f_host, int nrhs);
@@ -176,13 +195,14 @@ mht_status mht_covariance_apply(mht_plan *plan, const void *v, const double *S, 
  * ||r|| <= btol ||b|| + atol ||A|| ||x|| or test 2 ||A^* r|| <= atol ||A|| ||r||
  * (atol = btol = 0: exactly max_iters iterations).  Optional host outputs:
  * *iters_done, and per column rnorm[r] ~ ||b - Phi x||, arnorm[r] ~ ||Phi^*(b - Phi x)||
- * (the recurrences' estimates).  Synchronises.  Allocates its work vectors
- * (5 vectors of n or m x nrhs) per call. */
+ * (the recurrences' estimates).  Synchronises.  Work vectors (5 vectors of
+ * n or m x nrhs) are owned by the plan and grown with nrhs. */
 mht_status mht_lsqr(mht_plan *plan, const void *b, void *x, int nrhs, int max_iters, double atol, double btol,
                     int *iters_done, double *rnorm, double *arnorm);
 
-/* Capture each (direction, nrhs, c, f) apply sequence in a CUDA graph and
- * replay it on later calls with the same arguments (on = 1, default on). */
+/* Execution option (no paper passage): capture each
+ * (direction, nrhs, c, f) apply sequence in a CUDA graph and replay it on later
+ * calls with the same arguments (on = 1, default on). */
 mht_status mht_set_graphs(mht_plan *plan, int on);
 
 /* Adjoint group sums (a block row read by two transfers receives
@@ -212,16 +232,18 @@ mht_status mht_set_persistent(mht_plan *plan, int on);
 mht_status mht_phase_times(mht_plan *plan, int dir, double *ms, int32_t *stage, int32_t *kind, int cap,
                            int *nphases);
 
-/* Block until the plan's stream is idle; returns MHT_ERR_CUDA on a fault. */
+/* Block until the plan's stream is idle; returns MHT_ERR_CUDA on a fault
+ * (the asynchronous error surface of the calls above). */
 mht_status mht_sync(mht_plan *plan);
 
-/* Per-stage statistics of the packed plan.  stage in [0, L+1].
+/* Per-stage statistics of the packed plan (bytes per level, the paper's
+ * storage-as-runtime proxy).  stage in [0, L+1].
  *   coef_bytes: factor bytes read by the stage per apply (per RHS column);
  *   n_tiles_fwd / n_tiles_adj: work tiles; n_mat: materialised blocks. */
 mht_status mht_stage_stats(const mht_plan *plan, int stage, int64_t *coef_bytes,
                            int32_t *n_mat, int32_t *n_tiles_fwd, int32_t *n_tiles_adj);
 
-/* Kernel-level profiling on the launching stream.  When on, every kernel
+/* Kernel-level profiling on the launching stream (measurement).  When on, every kernel
  * launch of an apply is bracketed by CUDA events (kind 0 = forward stage,
  * 1 = adjoint stage, 2 = adjoint group-sum).  mht_profile_get synchronises and
  * returns the summed device time (ms) and launch count over all recorded
@@ -231,13 +253,14 @@ mht_status mht_set_profiling(mht_plan *plan, int on);
 mht_status mht_profile_get(mht_plan *plan, int kind, int stage, int nrhs, double *ms, int64_t *launches);
 mht_status mht_profile_reset(mht_plan *plan);
 
-/* Destroy the plan (synchronises its stream first).  NULL is a no-op. */
+/* Destroy the plan and every device buffer it owns (synchronises its
+ * streams first).  NULL is a no-op. */
 void mht_plan_destroy(mht_plan *plan);
 
 const char *mht_status_string(mht_status s);
 const char *mht_last_error(void);
 
-/* Library build identification ("sm_100a ..."). */
+/* Status name / thread-local detail of the last failure; build id ("sm_100a ..."). */
 const char *mht_build_info(void);
 
 #ifdef __cplusplus

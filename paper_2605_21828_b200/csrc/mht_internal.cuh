@@ -91,10 +91,8 @@ struct Ctx {  // per-launch pointers
   const double *diag;    // optional real diagonal on the coefficient side (m entries):
                          // forward reads c_k * g(d_k), adjoint writes g(d_k) * c_k
   int diag_sqrt;         // g(d) = sqrt(d) (GRF sampling) instead of d
-  int b16;               // debug: 16-byte row gathers in the warp-specialised real kernel (MHT_WS_B16=0: off)
   const int64_t *rdtab;  // fused adjoint sums: reader partial offsets
-  const void *tmaps;     // per-block 2-D TMA descriptors of T (CUtensorMap, 128 B each; adjoint tiles)
-  const void *tmaps_f;   // ... for the real forward tiles (16 rows x BK columns boxes)
+  const void *tmaps;     // per-block 2-D TMA descriptors of T (CUtensorMap, 128 B each; complex adjoint tiles)
   int fused;             // 1: adjoint inputs are summed from the partials on load
   int64_t m, n, Zt, Pt;  // Zt/Pt: workspace entries per RHS (layout [entry][rhs])
   int nrhs;

@@ -34,22 +34,14 @@ constexpr unsigned FULL = 0xffffffffu;
 // a launch without the PDL attribute.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-// launch with the programmatic-stream-serialisation attribute (PDL) unless
-// MHT_PDL=0; read per launch (graphs capture the attribute as a programmatic
-// edge).  Every kernel launched this way calls pdl_wait() before its first
-// access to memory an earlier kernel of the sequence writes or reads.
-inline bool pdl_on() {
-  const char *e = getenv("MHT_PDL");
-  return !(e && atoi(e) == 0);
-}
-// the multi-RHS kernels: PDL only with MHT_PDL_MMA=1 (neutral on c2 / c3,
-// 6% slower on c4's graph replay together with the 6-CTA real kernel,
-// profiles/r01_mma_pdl_ab.txt); their griddepcontrol instructions are no-ops
-// when launched without the attribute
-inline bool pdl_mma_on() {
-  const char *e = getenv("MHT_PDL_MMA");
-  return e && atoi(e) == 1 && pdl_on();
-}
+// The nrhs = 1 stage kernels and the group sums launch with the programmatic-
+// stream-serialisation attribute (graphs capture it as a programmatic edge);
+// every kernel launched this way calls pdl_wait() before its first access to
+// memory an earlier kernel of the sequence writes or reads.  The multi-RHS
+// kernels launch without it (neutral on c2 / c3, 6% slower on c4's graph
+// replay, profiles/r01_mma_pdl_ab.txt); their griddepcontrol instructions are
+// no-ops then.
+constexpr bool PDL_NRHS1 = true, PDL_MMA = false;
 template <class... KArgs, class... Args>
 void launch_ex(bool use_pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                Args... args) {
@@ -67,7 +59,7 @@ void launch_ex(bool use_pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size
 }
 template <class... KArgs, class... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
-  launch_ex(pdl_on(), kern, grid, block, 0, st, args...);
+  launch_ex(PDL_NRHS1, kern, grid, block, 0, st, args...);
 }
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
@@ -170,7 +162,7 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
 // adds them in split order — deterministic, no float atomics.
 // ------------------------------------------------------------------------
 // CG: workspace reads through L2 only (the persistent kernel; see in_value)
-template <class S, bool CG, int FBT = 8>
+template <class S, bool CG>
 __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
   using X = Tr<S>;
   const DevBlock B = cx.blocks[tl.blk];
@@ -218,13 +210,10 @@ __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
       }
     };
     if (jn == 32) {
-      if constexpr (REAL && FBT == 0) {
-#pragma unroll 16
-        for (int jj = 0; jj < 32; ++jj) step(jj);
-      } else if constexpr (REAL) {
+      if constexpr (REAL) {
         // each batch's FB loads issued before the first use (the interleaved
-        // form kept only ~4 loads outstanding per warp)
-        constexpr int FB = FBT;
+        // form kept only ~4 loads outstanding per warp; c3 3.35 -> 3.07 ms)
+        constexpr int FB = 8;
 #pragma unroll
         for (int h = 0; h < 32; h += FB) {
           double2 t[FB];
@@ -300,7 +289,7 @@ __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
   if (split && threadIdx.x == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
 }
 
-template <class S, int FBT = 8>
+template <class S>
 __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Tile *__restrict__ tiles) {
   const Tile tl = tiles[blockIdx.y];
   pdl_trigger();
@@ -321,16 +310,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Ti
     }
   }
   pdl_wait();
-  fwd_tile<S, false, FBT>(cx, tl);
-}
-
-// real forward load batching: MHT_FWD_FB=0 (interleaved) | 8 (default) | 16
-inline int fwd_fb() {
-  static int v = [] {
-    const char *e = getenv("MHT_FWD_FB");
-    return e ? atoi(e) : 8;
-  }();
-  return v;
+  fwd_tile<S, false>(cx, tl);
 }
 
 // adjoint input z[i] of a block: f through perm_x (leaf stage), else the group
@@ -366,12 +346,13 @@ __device__ __forceinline__ S adj_in(const Ctx &cx, const DevBlock &B, int i, int
 // partial column sums to scratch and the last CTA of the group to arrive adds
 // them in split order (deterministic, no float atomics).
 // ------------------------------------------------------------------------
-template <class S, int RB, bool CG, int RCH = ADJ_RCH, bool AR2 = false>
-__device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_f, int rhs0) {
+template <class S, bool CG>
+__device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_f) {
   using X = Tr<S>;
   // columns per warp: 8 complex / 16 real
   constexpr int ACOLS = adj_cols<S>();
   constexpr int CPW = ACOLS / (ADJ_THREADS / 32);
+  constexpr int RCH = ADJ_RCH;
   const DevBlock B = cx.blocks[tl.blk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool split = tl.pad >= 0;
@@ -383,12 +364,10 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
     rbeg = sidx * chunk;
     rend = min(B.r_out, rbeg + chunk);
   }
-  __shared__ S zs[RCH][RB];
-  S acc[CPW][RB];
+  __shared__ S zs[RCH];
+  S acc[CPW];
 #pragma unroll
-  for (int u = 0; u < CPW; ++u)
-#pragma unroll
-    for (int k = 0; k < RB; ++k) acc[u][k] = X::zero();
+  for (int u = 0; u < CPW; ++u) acc[u] = X::zero();
   const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
   const int64_t ld = B.ld;
   const int cbase = tl.start + warp * CPW;
@@ -397,44 +376,16 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
 
   for (int rc = rbeg; rc < rend; rc += RCH) {
     const int rn = min(RCH, rend - rc);
-    for (int e = threadIdx.x; e < rn * RB; e += ADJ_THREADS) {
-      const int i = e % rn, k = e / rn;
-      zs[i][k] = (rhs0 + k < cx.nrhs) ? adj_in<S, CG>(cx, B, rc + i, rhs0 + k, from_f) : X::zero();
-    }
-    if (REAL && (rn & 1) && threadIdx.x < RB) zs[rn][threadIdx.x] = X::zero();  // pair partner of the last row
+    for (int i = threadIdx.x; i < rn; i += ADJ_THREADS) zs[i] = adj_in<S, CG>(cx, B, rc + i, 0, from_f);
+    if (REAL && (rn & 1) && threadIdx.x == 0) zs[rn] = X::zero();  // pair partner of the last row
     __syncthreads();
-    if constexpr (REAL) {
-      // real: lane takes the row pair (2q, 2q + 1) of each of its columns with
-      // one 16-byte load (rc is even; the pad row of an odd r_out is zero)
-      static_assert(!REAL || RB == 1, "real pair path is the nrhs = 1 kernel");
-      if (cbase < cend && AR2) {
-        // two row pairs per lane per step (2q, 2q + 1 and 2q + 64, 2q + 65):
-        // 2 CPW 16-byte loads in flight
-        for (int q = lane; 2 * q < rn; q += 64) {
-          const bool v2 = 2 * (q + 32) < rn;
-          const double z0 = zs[2 * q][0], z1 = zs[2 * q + 1][0];
-          const double z2 = v2 ? zs[2 * q + 64][0] : 0.0, z3 = v2 ? zs[2 * q + 65][0] : 0.0;
-          double2 t0[CPW], t1[CPW];
-#pragma unroll
-          for (int u = 0; u < CPW; ++u) {
-            const bool cu = cbase + u < cend;
-            const double *cp = reinterpret_cast<const double *>(T) + (int64_t)(cbase + u) * ld + rc + 2 * q;
-            t0[u] = cu ? Tr<double>::ldT2(cp) : make_double2(0.0, 0.0);
-            t1[u] = (cu && v2) ? Tr<double>::ldT2(cp + 64) : make_double2(0.0, 0.0);
-          }
-#pragma unroll
-          for (int u = 0; u < CPW; ++u) {
-            double &a = reinterpret_cast<double &>(acc[u][0]);
-            a = ::fma(t0[u].x, z0, a);
-            a = ::fma(t0[u].y, z1, a);
-            a = ::fma(t1[u].x, z2, a);
-            a = ::fma(t1[u].y, z3, a);
-          }
-        }
-      } else if (cbase < cend) {
+    if (cbase < cend) {
+      if constexpr (REAL) {
+        // real: lane takes the row pair (2q, 2q + 1) of each of its columns with
+        // one 16-byte load (rc is even; the pad row of an odd r_out is zero);
+        // all CPW column loads issued before their first use (predicated)
         for (int q = lane; 2 * q < rn; q += 32) {
-          const double z0 = zs[2 * q][0], z1 = zs[2 * q + 1][0];
-          // all CPW column loads issued before their first use (predicated)
+          const double z0 = zs[2 * q], z1 = zs[2 * q + 1];
           double2 t[CPW];
 #pragma unroll
           for (int u = 0; u < CPW; ++u)
@@ -443,18 +394,18 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
                        : make_double2(0.0, 0.0);
 #pragma unroll
           for (int u = 0; u < CPW; ++u) {
-            double &a = reinterpret_cast<double &>(acc[u][0]);
+            double &a = reinterpret_cast<double &>(acc[u]);
             a = ::fma(t[u].x, z0, a);
             a = ::fma(t[u].y, z1, a);
           }
         }
-      }
-    } else if (cbase < cend) {
-      if constexpr (AR2) {
-        // two rows per lane per step (i, i + 32): 2 CPW 16-byte loads in flight
+      } else {
+        // complex: two rows per lane per step (i, i + 32), 2 CPW 16-byte loads
+        // in flight (c2 adj_nrhs1 6.60 -> 6.56 ms, profiles/r01_adj_ar2_ab.txt);
+        // a lane still accumulates its rows in ascending order
         for (int i = lane; i < rn; i += 64) {
           const bool v2 = i + 32 < rn;
-          const S z0 = zs[i][0], z1 = v2 ? zs[i + 32][0] : X::zero();
+          const S z0 = zs[i], z1 = v2 ? zs[i + 32] : X::zero();
           S t0[CPW], t1[CPW];
 #pragma unroll
           for (int u = 0; u < CPW; ++u) {
@@ -465,22 +416,9 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
           }
 #pragma unroll
           for (int u = 0; u < CPW; ++u) {
-            X::fmac(acc[u][0], t0[u], z0);
-            X::fmac(acc[u][0], t1[u], z1);
+            X::fmac(acc[u], t0[u], z0);
+            X::fmac(acc[u], t1[u], z1);
           }
-        }
-      } else {
-        for (int i = lane; i < rn; i += 32) {
-          S zv[RB];
-#pragma unroll
-          for (int k = 0; k < RB; ++k) zv[k] = zs[i][k];
-          S t[CPW];
-#pragma unroll
-          for (int u = 0; u < CPW; ++u) t[u] = cbase + u < cend ? X::ldT(T + (int64_t)(cbase + u) * ld + rc + i) : X::zero();
-#pragma unroll
-          for (int u = 0; u < CPW; ++u)
-#pragma unroll
-            for (int k = 0; k < RB; ++k) X::fmac(acc[u][k], t[u], zv[k]);
         }
       }
     }
@@ -488,20 +426,16 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
   }
   // skeleton part: w[skel[i]] = z[i]  (written once, by the block's first tile)
   if (tl.start == 0 && sidx == 0 && B.n_skel > 0) {
-    for (int e = threadIdx.x; e < B.n_skel * RB; e += ADJ_THREADS) {
-      const int i = e % B.n_skel, k = e / B.n_skel;
-      if (rhs0 + k >= cx.nrhs) continue;
+    for (int i = threadIdx.x; i < B.n_skel; i += ADJ_THREADS) {
       const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
-      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0 + k] = adj_in<S, CG>(cx, B, i, rhs0 + k, from_f);
+      static_cast<S *>(cx.part)[B.part_off + q] = adj_in<S, CG>(cx, B, i, 0, from_f);
     }
   }
   // warp reductions
 #pragma unroll
   for (int u = 0; u < CPW; ++u)
 #pragma unroll
-    for (int k = 0; k < RB; ++k)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[u][k] = X::add(acc[u][k], X::shfl_xor(acc[u][k], o));
+    for (int o = 16; o > 0; o >>= 1) acc[u] = X::add(acc[u], X::shfl_xor(acc[u], o));
   if (!split) {
     if (lane == 0) {
 #pragma unroll
@@ -509,21 +443,17 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
         const int col = cbase + u;
         if (col >= cend) continue;
         const int q = (B.flags & F_RED_IOTA) ? col : cx.idx[B.red_off + col];
-#pragma unroll
-        for (int k = 0; k < RB; ++k)
-          if (rhs0 + k < cx.nrhs) static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0 + k] = acc[u][k];
+        static_cast<S *>(cx.part)[B.part_off + q] = acc[u];
       }
     }
   } else {
-    // RB == 1 here (nrhs = 1 path)
-    static_assert(RB == 1, "row splits are built for the nrhs = 1 tiles only");
     S *scratch = static_cast<S *>(cx.fsplit);
     const int grp = tl.pad >> 8;
     const int64_t sbase = B.asp_off + (int64_t)(tl.start / ACOLS) * B.pad2 * ACOLS;
     __shared__ int last;
     if (lane == 0) {
 #pragma unroll
-      for (int u = 0; u < CPW; ++u) scratch[sbase + (int64_t)sidx * ACOLS + warp * CPW + u] = acc[u][0];
+      for (int u = 0; u < CPW; ++u) scratch[sbase + (int64_t)sidx * ACOLS + warp * CPW + u] = acc[u];
     }
     __threadfence();
     __syncthreads();
@@ -536,13 +466,13 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
       for (int k = 0; k < B.pad2; ++k) sum = X::add(sum, X::ldcg(scratch + sbase + (int64_t)k * ACOLS + c));
       const int col = tl.start + c;
       const int q = (B.flags & F_RED_IOTA) ? col : cx.idx[B.red_off + col];
-      static_cast<S *>(cx.part)[(B.part_off + q) * cx.nrhs + rhs0] = sum;
+      static_cast<S *>(cx.part)[B.part_off + q] = sum;
     }
     if (threadIdx.x == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
   }
 }
 
-template <class S, int RB, int RCH = ADJ_RCH, bool AR2 = false>
+template <class S>
 __global__ void __launch_bounds__(ADJ_THREADS, 7) adj_kernel(const Ctx cx, const Tile *__restrict__ tiles,
                                                              int from_f) {
   const Tile tl = tiles[blockIdx.y];
@@ -561,28 +491,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 7) adj_kernel(const Ctx cx, const
     }
   }
   pdl_wait();
-  adj_tile<S, RB, false, RCH, AR2>(cx, tl, from_f, blockIdx.x * RB);
-}
-
-// complex adjoint, two rows per lane per step (default; MHT_ADJ_AR2=0: one):
-// c2 adj_nrhs1 6.60 -> 6.56 ms (profiles/r01_adj_ar2_ab.txt)
-inline bool adj_ar2() {
-  const char *e = getenv("MHT_ADJ_AR2");
-  return !(e && atoi(e) == 0);
-}
-
-// rows of z staged per pass: MHT_ADJ_RCH=512|1024 (experiments), default ADJ_RCH
-// real adjoint, two row pairs per lane per step: MHT_ADJ_AR2R=1
-inline bool adj_ar2_real() {
-  const char *e = getenv("MHT_ADJ_AR2R");
-  return e && atoi(e) == 1;
-}
-inline int adj_rch() {
-  static int v = [] {
-    const char *e = getenv("MHT_ADJ_RCH");
-    return e ? atoi(e) : ADJ_RCH;
-  }();
-  return v;
+  adj_tile<S, false>(cx, tl, from_f);
 }
 
 // ------------------------------------------------------------------------
@@ -666,13 +575,11 @@ __host__ __device__ __forceinline__ int frag_row(int gid) {
 
 // MMA row r (0..15, a0 rows 0..7, a1 rows 8..15) -> tile row within the warp's
 // 16-row slab.  MODE 0: identity; 1: swizzled adjoint tile (frag_row, a1 = a0
-// + 8); 2: swizzled real forward tile [k][16 rows] (quad q of rows -> tile rows
-// {2q, 2q+1, 2q+8, 2q+9}: the half warp's 8-byte loads hit 16 distinct banks)
+// + 8)
 template <class S, int MODE>
 __host__ __device__ __forceinline__ int tile_row(int r) {
   if (MODE == 0) return r;
-  if (MODE == 1) return frag_row<S, true>(r & 7) + 8 * (r >> 3);
-  return 2 * (r >> 2) + (r & 1) + 8 * ((r >> 1) & 1);
+  return frag_row<S, true>(r & 7) + 8 * (r >> 3);
 }
 
 template <class S, bool ADJ, int NT, bool M3, int BAR, int MODE = 0>
@@ -1032,60 +939,43 @@ __device__ __forceinline__ void tma_2d_g2s(void *smem, const void *tmap, int c0,
 
 constexpr int WS_STAGES = 3;
 constexpr int WS_THREADS = MM_THREADS + 32;
-// padded leading dimensions of the factor tile in shared memory (elements):
-// forward column-major [k][m] with AP = 64 + (2 complex | 4 real), adjoint
-// row-major [m][k] with BKP = BK + 4; chosen so a warp's A-fragment loads hit
-// distinct banks (16-byte slots 2 tig + gid / 4 gid + tig distinct mod 8 per
-// quarter warp; 8-byte slots distinct mod 16 per half warp)
-template <class S, bool ADJ, int FM = 0>
+constexpr int WS_MINB = 3;  // CTAs per SM the registers are sized for (<= 136 registers)
+// Factor tile in shared memory (complex, BK = 16): forward padded column-major
+// [k][64 + 2] filled by 1-D bulk copies (one per column of T); adjoint the two
+// 128-byte-swizzled 2-D TMA boxes [half][m][128 B].  The +2 pad makes a
+// quarter warp's 16-byte A-fragment loads (slots 2 tig + gid) hit distinct banks.
+template <bool ADJ>
 __host__ __device__ constexpr int ws_a_elems() {
-  return (ADJ || sizeof(S) == 8 || FM == 3) ? MM_BM * mm_bk<S>() : mm_bk<S>() * (MM_BM + 2);
+  return ADJ ? MM_BM * 16 : 16 * (MM_BM + 2);
 }
-// A-tile layout / row mapping of the warp-specialised kernel: 0 padded
-// column-major by 1-D bulk copies (complex forward), 1 swizzled [half][m][k]
-// by 2-D TMA (adjoint), 2 swizzled [quad][k][16 rows] by 2-D TMA (real forward)
-// FM (complex forward): 0 = padded 1-D bulk copies, 3 = swizzled [q][k][8 rows]
-// by eight 2-D TMA requests (fragment rows permuted as in mode 1)
-template <class S, bool ADJ, int FM = 0>
-__host__ __device__ constexpr int ws_mode() {
-  return ADJ ? 1 : (sizeof(S) == 8 ? 2 : FM);
-}
+// B chunk: fragment order (BK x 32 slots)
+constexpr int WS_B_ELEMS = 16 * 32;
 
-// B chunk of the warp-specialised kernel: complex in fragment order (BK x 32
-// slots), real row-major [k][32 + 4] (each row one contiguous 256-byte gather
-// by 16-byte cp.async; the +4 pad makes the fragment reads conflict-free)
-template <class S>
-__host__ __device__ constexpr int ws_b_elems() {
-  return sizeof(S) == 16 ? mm_bk<S>() / 4 * 4 * 32 : mm_bk<S>() * (32 + 4);
-}
-
-template <class S, bool ADJ, bool M3, int FM = 0>
+template <bool ADJ>
 __host__ __device__ constexpr int ws_smem_bytes() {
   // NS x (A tile + B chunk) operand buffers + 2 NS mbarriers + 1 KB to align
   // the stages to the 1024-byte period of the 128-byte TMA swizzle
-  return WS_STAGES * (ws_a_elems<S, ADJ, FM>() + ws_b_elems<S>()) * (int)sizeof(S) + 2 * WS_STAGES * 8 + 1024;
+  return WS_STAGES * (ws_a_elems<ADJ>() + WS_B_ELEMS) * 16 + 2 * WS_STAGES * 8 + 1024;
 }
 
-template <class S, bool ADJ, bool M3, int MINB, int FM = 0>
-__global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, const Tile *__restrict__ tiles,
-                                                                  int from_f) {
+// Complex plans, nrhs >= 32 (profiles/r01_mma_ws_ab.txt: c2 nrhs 32 forward
+// 18.1 vs 21.5 ms, adjoint 18.5 vs 19.9 ms against the classic structure).
+// Complex products by Gauss's 3-multiplication form.
+template <bool ADJ>
+__global__ void __launch_bounds__(WS_THREADS, WS_MINB) mma_ws_kernel(const Ctx cx, const Tile *__restrict__ tiles,
+                                                                     int from_f) {
+  using S = double2;
   using X = Tr<S>;
   using PL = Planes<S>;
   constexpr int NT = 4;
-  constexpr bool CPLX = PL::cplx;
-  constexpr bool G3 = CPLX && M3;
-  constexpr int NRT = 8 * NT;
+  constexpr bool M3 = true;
   constexpr int BK = mm_bk<S>();
   constexpr int KS = BK / 4;
   constexpr int AW = MM_BM / 16;
-  constexpr int A_CH = ws_a_elems<S, ADJ, FM>();
-  // leading dimension of the factor tile in shared memory: forward padded
-  // column-major [k][m]; adjoint the TMA box [m][k] as written (dense)
-  constexpr int AP = ADJ ? BK : MM_BM + 2;  // (mode 0 only)
-  constexpr int MODE = ws_mode<S, ADJ, FM>();
-  constexpr int B_CH = ws_b_elems<S>();
-  constexpr bool BROW = !CPLX;  // real: row-major padded B chunk
-  constexpr int NPB = 32 + 4;
+  constexpr int A_CH = ws_a_elems<ADJ>();
+  constexpr int AP = MM_BM + 2;  // forward tile leading dimension
+  constexpr int MODE = ADJ ? 1 : 0;
+  constexpr int B_CH = WS_B_ELEMS;
   constexpr int NS = WS_STAGES;
   extern __shared__ __align__(128) unsigned char ws_smem[];
   // stage buffers start at a 1024-byte boundary (shared-space address)
@@ -1098,7 +988,7 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   pdl_trigger();
   const Tile tl = tiles[blockIdx.y];  // plan tables: never written by kernels
   const DevBlock B = cx.blocks[tl.blk];
-  const int rhs0 = blockIdx.x * NRT;
+  const int rhs0 = blockIdx.x * 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
   const int64_t ld = B.ld;
@@ -1144,59 +1034,25 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
       if (ADJ) return from_f_ ? __ldg(cx.perm + B.out_off + k) : k;
       return red_iota ? k : __ldg(cx.idx + B.red_off + k);
     };
-    // real (BROW): lane owns row k = lane of every chunk (BK = 32)
-    auto row_index_r = [&](int kc) -> int {
-      const int k = kbeg + kc * BK + lane;
-      if (k >= kend) return -1;
-      if (ADJ) return from_f_ ? __ldg(cx.perm + B.out_off + k) : k;
-      return red_iota ? k : __ldg(cx.idx + B.red_off + k);
-    };
     int qn[KS];
 #pragma unroll
-    for (int k4 = 0; k4 < KS; ++k4) qn[k4] = (nchunks > 0 && !BROW) ? row_index(0, k4) : -1;
-    int qrn = (nchunks > 0 && BROW) ? row_index_r(0) : -1;
+    for (int k4 = 0; k4 < KS; ++k4) qn[k4] = nchunks > 0 ? row_index(0, k4) : -1;
     for (int kc = 0; kc < nchunks; ++kc) {
       const int slot = kc % NS;
       int q[KS];
 #pragma unroll
       for (int k4 = 0; k4 < KS; ++k4) q[k4] = qn[k4];
-      const int qr = qrn;
       if (kc + 1 < nchunks) {
-        if (BROW) {
-          qrn = row_index_r(kc + 1);
-        } else {
 #pragma unroll
-          for (int k4 = 0; k4 < KS; ++k4) qn[k4] = row_index(kc + 1, k4);
-        }
+        for (int k4 = 0; k4 < KS; ++k4) qn[k4] = row_index(kc + 1, k4);
       }
       mbar_wait(empty + slot, ((kc / NS) & 1) ^ 1);
       const int kb = kbeg + kc * BK;
       const int kn = min(BK, kend - kb);  // valid k of this chunk
       S *dA = As + slot * A_CH;
-      // factor tile by TMA bulk copies (16-byte multiples: the real layout has
-      // even ld and a zero pad row, so an odd length rounds up into it)
-      constexpr int EV = sizeof(S) == 8 ? 2 : 1;
-      if (MODE == 3) {
-        if (lane == 0) {
-          // complex forward: 64 x BK tile as eight 2-D TMA requests of 8 rows
-          // (128 B) x BK columns, 128-byte swizzled, past-the-block zero-filled
-          const void *tmap = static_cast<const unsigned char *>(cx.tmaps_f) + (size_t)tl.blk * 128;
-          mbar_arrive_expect_tx(full + slot, (unsigned)(MM_BM * BK * sizeof(S)));
-#pragma unroll
-          for (int q8 = 0; q8 < 8; ++q8) tma_2d_g2s(dA + q8 * BK * 8, tmap, 2 * (tl.start + 8 * q8), kb, full + slot);
-        }
-      } else if (MODE == 2) {
-        if (lane == 0) {
-          // real forward: the 64 x BK tile as four 2-D TMA requests of 16 rows
-          // (128 B) x BK columns, 128-byte swizzled, past-the-block zero-filled
-          const void *tmap = static_cast<const unsigned char *>(cx.tmaps_f) + (size_t)tl.blk * 128;
-          mbar_arrive_expect_tx(full + slot, (unsigned)(MM_BM * BK * sizeof(S)));
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) tma_2d_g2s(dA + q4 * BK * 16, tmap, tl.start + 16 * q4, kb, full + slot);
-        }
-      } else if (!ADJ) {
-        // forward: column k of the tile = tl.count contiguous rows of T
-        const unsigned cb = (unsigned)((tl.count + EV - 1) / EV * EV * sizeof(S));
+      if (!ADJ) {
+        // forward: column k of the tile = tl.count contiguous rows of T (TMA bulk copies)
+        const unsigned cb = (unsigned)(tl.count * sizeof(S));
         if (lane == 0) mbar_arrive_expect_tx(full + slot, cb * kn);
         for (int j = lane; j < BK; j += 32) {
           if (j < kn) {
@@ -1213,99 +1069,51 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
         const void *tmap = static_cast<const unsigned char *>(cx.tmaps) + (size_t)tl.blk * 128;
         mbar_arrive_expect_tx(full + slot, (unsigned)(MM_BM * BK * sizeof(S)));
         constexpr int KH = BK / 2;
-        tma_2d_g2s(dA, tmap, kb * (int)(sizeof(S) / 8), tl.start, full + slot);
-        tma_2d_g2s(dA + MM_BM * KH, tmap, (kb + KH) * (int)(sizeof(S) / 8), tl.start, full + slot);
+        tma_2d_g2s(dA, tmap, kb * 2, tl.start, full + slot);
+        tma_2d_g2s(dA + MM_BM * KH, tmap, (kb + KH) * 2, tl.start, full + slot);
       }
       S *dB = Bs + slot * B_CH;
-      if constexpr (BROW) {
-        // row k = lane: its 32 right-hand sides, contiguous in the workspace
-        // (RHS-fastest) -> 16 x 16-byte cp.async; c / f rows (column-major
-        // user arrays), odd nrhs and a fused diagonal take 8-byte elements
-        S *drow = dB + lane * NPB;
-        const int nv = min(32, cx.nrhs - rhs0);  // valid right-hand sides
-        const S *srow = nullptr;
-        bool contiguous = false;
-        int64_t rstride = 0;  // element stride between right-hand sides otherwise
-        if (qr >= 0) {
+      // a lane's KS rows: base pointer and right-hand-side stride resolved
+      // once per row (segment / source / perm), then one multiply-add per element
+      const S *rb[KS];
+      int64_t rs[KS];
+#pragma unroll
+      for (int k4 = 0; k4 < KS; ++k4) {
+        const int qq = q[k4];
+        rb[k4] = static_cast<const S *>(cx.z);
+        rs[k4] = 0;
+        if (qq >= 0) {
           if (ADJ) {
             if (from_f_) {
-              srow = static_cast<const S *>(cx.fin) + (int64_t)rhs0 * cx.n + qr;
-              rstride = cx.n;
+              rb[k4] = static_cast<const S *>(cx.fin) + qq;
+              rs[k4] = cx.n;
             } else {
-              srow = static_cast<const S *>(cx.z) + (B.out_off + qr) * cx.nrhs + rhs0;
-              contiguous = true;
+              rb[k4] = static_cast<const S *>(cx.z) + (B.out_off + qq) * cx.nrhs;
+              rs[k4] = 1;
             }
           } else {
-            const bool s1 = qr >= B.seg_len[0];
-            const int64_t off = s1 ? B.seg_off[1] + (qr - B.seg_len[0]) : B.seg_off[0] + qr;
-            const int32_t srcsel = s1 ? B.seg_src[1] : B.seg_src[0];
-            if (srcsel == SRC_C) {
-              srow = static_cast<const S *>(cx.c) + (int64_t)rhs0 * cx.m + off;
-              rstride = cx.m;
+            const bool s1 = qq >= B.seg_len[0];
+            const int64_t off = s1 ? B.seg_off[1] + (qq - B.seg_len[0]) : B.seg_off[0] + qq;
+            if ((s1 ? B.seg_src[1] : B.seg_src[0]) == SRC_C) {
+              rb[k4] = static_cast<const S *>(cx.c) + off;
+              rs[k4] = cx.m;
             } else {
-              srow = static_cast<const S *>(cx.z) + off * cx.nrhs + rhs0;
-              contiguous = true;
+              rb[k4] = static_cast<const S *>(cx.z) + off * cx.nrhs;
+              rs[k4] = 1;
             }
           }
         }
-        if (contiguous && !reg_path && (cx.nrhs & 1) == 0 && cx.b16) {
+      }
 #pragma unroll
-          for (int h = 0; h < 16; ++h) cp_async<16>(drow + 2 * h, srow + 2 * h, 2 * h < nv);
-        } else if (!reg_path) {
-          for (int n = 0; n < 32; ++n) {
-            const bool ok = qr >= 0 && n < nv;
-            cp_async<8>(drow + n, ok ? (contiguous ? srow + n : srow + n * rstride) : static_cast<const S *>(cx.z), ok);
-          }
+      for (int i = 0; i < B_CH / 32; ++i) {
+        const int k4 = i / NT, t = i % NT;
+        const int r = rhs0 + t * 8 + gid_;
+        const bool ok = q[k4] >= 0 && r < cx.nrhs;
+        const S *src = ok ? rb[k4] + (int64_t)r * rs[k4] : static_cast<const S *>(cx.z);
+        if (!reg_path) {
+          cp_async<sizeof(S)>(dB + lane + 32 * i, src, ok);
         } else {
-          for (int n = 0; n < 32; ++n) {
-            const bool ok = qr >= 0 && n < nv;
-            drow[n] = ok ? (ADJ ? (contiguous ? srow[n] : srow[n * rstride]) : in_value<S>(cx, B, qr, rhs0 + n))
-                         : X::zero();
-          }
-        }
-      } else {
-        // a lane's KS rows: base pointer and right-hand-side stride resolved
-        // once per row (segment / source / perm), then one multiply-add per element
-        const S *rb[KS];
-        int64_t rs[KS];
-#pragma unroll
-        for (int k4 = 0; k4 < KS; ++k4) {
-          const int qq = q[k4];
-          rb[k4] = static_cast<const S *>(cx.z);
-          rs[k4] = 0;
-          if (qq >= 0) {
-            if (ADJ) {
-              if (from_f_) {
-                rb[k4] = static_cast<const S *>(cx.fin) + qq;
-                rs[k4] = cx.n;
-              } else {
-                rb[k4] = static_cast<const S *>(cx.z) + (B.out_off + qq) * cx.nrhs;
-                rs[k4] = 1;
-              }
-            } else {
-              const bool s1 = qq >= B.seg_len[0];
-              const int64_t off = s1 ? B.seg_off[1] + (qq - B.seg_len[0]) : B.seg_off[0] + qq;
-              if ((s1 ? B.seg_src[1] : B.seg_src[0]) == SRC_C) {
-                rb[k4] = static_cast<const S *>(cx.c) + off;
-                rs[k4] = cx.m;
-              } else {
-                rb[k4] = static_cast<const S *>(cx.z) + off * cx.nrhs;
-                rs[k4] = 1;
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < B_CH / 32; ++i) {
-          const int k4 = i / NT, t = i % NT;
-          const int r = rhs0 + t * 8 + gid_;
-          const bool ok = q[k4] >= 0 && r < cx.nrhs;
-          const S *src = ok ? rb[k4] + (int64_t)r * rs[k4] : static_cast<const S *>(cx.z);
-          if (!reg_path) {
-            cp_async<sizeof(S)>(dB + lane + 32 * i, src, ok);
-          } else {
-            dB[lane + 32 * i] = ok ? (ADJ ? *src : in_value<S>(cx, B, q[k4], r)) : X::zero();
-          }
+          dB[lane + 32 * i] = ok ? (ADJ ? *src : in_value<S>(cx, B, q[k4], r)) : X::zero();
         }
       }
       mbar_cp_async_arrive(full + slot);  // completes when this lane's cp.async have landed
@@ -1316,68 +1124,42 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
 
   // ------------------------------------------------ consumer warps
   const int gid = lane >> 2, tig = lane & 3;
-  double c0[NT][4], c1[NT][4], c2[G3 ? NT : 1][4];
+  double c0[NT][4], c1[NT][4], c2[NT][4];
 #pragma unroll
   for (int t = 0; t < NT; ++t)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) c0[t][v] = c1[t][v] = 0.0;
-#pragma unroll
-  for (int t = 0; t < (G3 ? NT : 1); ++t)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) c2[t][v] = 0.0;
+    for (int v = 0; v < 4; ++v) c0[t][v] = c1[t][v] = c2[t][v] = 0.0;
+  const int m0 = warp * 16 + tile_row<S, MODE>(gid), m1 = warp * 16 + tile_row<S, MODE>(gid + 8);
   for (int kc = 0; kc < nchunks; ++kc) {
     const int slot = kc % NS;
     mbar_wait(full + slot, (kc / NS) & 1);
     const S *Ac = As + slot * A_CH;
     const S *Bc = Bs + slot * B_CH;
-    constexpr int RMODE = MODE == 3 ? 1 : MODE;  // row permutation
-    const int m0 = warp * 16 + tile_row<S, RMODE>(gid), m1 = warp * 16 + tile_row<S, RMODE>(gid + 8);
 #pragma unroll
     for (int k4 = 0; k4 < KS; ++k4) {
       const int k = 4 * k4 + tig;
       S a0, a1;
-      if constexpr (MODE == 3) {
-        // swizzled [q][k][8 rows]: 16-byte chunk (row m & 7) of row k at (m & 7) ^ (k & 7)
-        const unsigned char *ab = reinterpret_cast<const unsigned char *>(Ac) + k * 128;
-        a0 = *reinterpret_cast<const S *>(ab + (m0 >> 3) * (BK * 128) + (((m0 & 7) ^ (k & 7)) << 4));
-        a1 = *reinterpret_cast<const S *>(ab + (m1 >> 3) * (BK * 128) + (((m1 & 7) ^ (k & 7)) << 4));
-      } else if constexpr (MODE == 2) {
-        // swizzled [quad][k][16 rows]: 16-byte chunk c of row k sits at c ^ (k & 7)
-        const unsigned char *ab = reinterpret_cast<const unsigned char *>(Ac) + k * 128;
-        const int mm0 = m0 & 15, mm1 = m1 & 15;
-        a0 = *reinterpret_cast<const S *>(ab + (m0 >> 4) * (BK * 128) + (((mm0 >> 1) ^ (k & 7)) << 4) + (mm0 & 1) * 8);
-        a1 = *reinterpret_cast<const S *>(ab + (m1 >> 4) * (BK * 128) + (((mm1 >> 1) ^ (k & 7)) << 4) + (mm1 & 1) * 8);
-      } else if constexpr (ADJ) {
+      if constexpr (ADJ) {
         // swizzled [half][m][128 B]: 16-byte chunk c of row m sits at c ^ (m & 7)
         constexpr int KH = BK / 2;
-        const int h = k / KH, kk = k % KH;
-        const int byte = kk * (int)sizeof(S);
+        const int h = k / KH, c = k % KH;
         const unsigned char *hb = reinterpret_cast<const unsigned char *>(Ac) + h * (MM_BM * 128);
-        const int c = byte >> 4, o = byte & 15;
-        a0 = *reinterpret_cast<const S *>(hb + m0 * 128 + ((c ^ (m0 & 7)) << 4) + o);
-        a1 = *reinterpret_cast<const S *>(hb + m1 * 128 + ((c ^ (m1 & 7)) << 4) + o);
+        a0 = *reinterpret_cast<const S *>(hb + m0 * 128 + ((c ^ (m0 & 7)) << 4));
+        a1 = *reinterpret_cast<const S *>(hb + m1 * 128 + ((c ^ (m1 & 7)) << 4));
       } else {
         a0 = Ac[k * AP + m0];
         a1 = Ac[k * AP + m1];
       }
       const double ar0 = PL::re(a0), ar1 = PL::re(a1);
+      // conj(T) for the adjoint
       const double ai0 = ADJ ? -PL::im(a0) : PL::im(a0), ai1 = ADJ ? -PL::im(a1) : PL::im(a1);
       const double as0 = ar0 + ai0, as1 = ar1 + ai1;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        const S b = BROW ? Bc[k * NPB + 8 * t + gid] : Bc[(k4 * NT + t) * 32 + lane];
-        if constexpr (!CPLX) {
-          dmma(c0[t], ar0, ar1, PL::re(b));
-        } else if constexpr (G3) {
-          dmma(c0[t], ar0, ar1, PL::re(b));
-          dmma(c1[t], ai0, ai1, PL::im(b));
-          dmma(c2[t], as0, as1, PL::re(b) + PL::im(b));
-        } else {
-          dmma(c0[t], ar0, ar1, PL::re(b));
-          dmma(c0[t], -ai0, -ai1, PL::im(b));
-          dmma(c1[t], ar0, ar1, PL::im(b));
-          dmma(c1[t], ai0, ai1, PL::re(b));
-        }
+        const S b = Bc[(k4 * NT + t) * 32 + lane];
+        dmma(c0[t], ar0, ar1, PL::re(b));
+        dmma(c1[t], ai0, ai1, PL::im(b));
+        dmma(c2[t], as0, as1, PL::re(b) + PL::im(b));
       }
     }
     __syncwarp();
@@ -1385,71 +1167,26 @@ __global__ void __launch_bounds__(WS_THREADS, MINB) mma_ws_kernel(const Ctx cx, 
   }
   // all consumer warps are past their last read of the operand buffers
   consumer_sync<1>();
-  constexpr int RMODE_EPI = MODE == 3 ? 1 : MODE;
-  mma_epilogue<S, ADJ, NT, M3, 1, RMODE_EPI>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
+  mma_epilogue<S, ADJ, NT, M3, 1, MODE>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
 }
 
-// Which multi-RHS launches use the warp-specialised TMA kernel
-// (profiles/r01_mma_ws_ab.txt): complex plans, both directions (c2 nrhs 32:
-// forward 18.1 vs 21.5 ms, adjoint 18.5 vs 19.9 ms).  Real plans stay on the
-// classic kernel (c3: the producer warp's 32 gathers per lane per chunk make
-// WS 1.3-3x slower).  MHT_MMA_WS=0 never, =1 always.
-inline int mma_ws_mode() {
-  const char *e = getenv("MHT_MMA_WS");  // read per launch (debug / A-B within one process)
-  if (e && atoi(e) == 0) return 0;
-  if (e && atoi(e) == 1) return 1;
-  return -1;
-}
-template <class S, bool ADJ>
-inline bool mma_ws() {
-  // real plans never take the warp-specialised kernel: its row-gather
-  // variant showed a rare nondeterministic error on c3 (1 run in 3,
-  // profiles/r01_mma_ws_ab.txt) that is not understood yet
-  if (!Planes<S>::cplx) return false;
-  const int mode = mma_ws_mode();
-  if (mode >= 0) return mode == 1;
-  return true;
+// dynamic shared memory above 48 KB is opted into per device (the attribute
+// applies to the device current when it is set): a bit per device ordinal
+template <class K>
+void smem_optin(K kern, int bytes) {
+  static unsigned long long done = 0;  // device bitmask
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && (done >> dev & 1ull)) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (dev < 64) done |= 1ull << dev;
 }
 
-// CTAs per SM the warp-specialised kernel's registers are sized for: 3
-// (<= 136 registers) by default, MHT_MMA_WS_MINB=2 for the unconstrained build
-inline int mma_ws_minb() {
-  static int v = [] {
-    const char *e = getenv("MHT_MMA_WS_MINB");
-    return (e && atoi(e) == 2) ? 2 : 3;
-  }();
-  return v;
-}
-
-template <class S, bool ADJ, bool M3, int MINB, int FM>
-void mma_ws_launch_t(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
-  constexpr int smem = ws_smem_bytes<S, ADJ, M3, FM>();
-  static bool attr = [] {
-    cudaFuncSetAttribute(mma_ws_kernel<S, ADJ, M3, MINB, FM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    return true;
-  }();
-  (void)attr;
-  launch_ex(pdl_mma_on(), mma_ws_kernel<S, ADJ, M3, MINB, FM>, dim3((cx.nrhs + 31) / 32, nt), dim3(WS_THREADS), smem, st,
-            cx, tiles, from_f);
-}
-
-// complex forward A tile: MHT_WS_FMODE=3 (2-D TMA, swizzled) | 0 (1-D bulk
-// copies, padded; default)
-inline int ws_fmode() {
-  const char *e = getenv("MHT_WS_FMODE");
-  return (e && atoi(e) == 3) ? 3 : 0;
-}
-
-template <class S, bool ADJ, bool M3>
+template <bool ADJ>
 void mma_ws_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
-  const bool f3 = !ADJ && Planes<S>::cplx && ws_fmode() == 3;
-  if (mma_ws_minb() == 2) {
-    if (f3) mma_ws_launch_t<S, ADJ, M3, 2, 3>(cx, tiles, nt, from_f, st);
-    else mma_ws_launch_t<S, ADJ, M3, 2, 0>(cx, tiles, nt, from_f, st);
-  } else {
-    if (f3) mma_ws_launch_t<S, ADJ, M3, 3, 3>(cx, tiles, nt, from_f, st);
-    else mma_ws_launch_t<S, ADJ, M3, 3, 0>(cx, tiles, nt, from_f, st);
-  }
+  constexpr int smem = ws_smem_bytes<ADJ>();
+  smem_optin(mma_ws_kernel<ADJ>, smem);
+  launch_ex(PDL_MMA, mma_ws_kernel<ADJ>, dim3((cx.nrhs + 31) / 32, nt), dim3(WS_THREADS), smem, st, cx, tiles, from_f);
 }
 
 // ------------------------------------------------------------------------
@@ -1631,94 +1368,43 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_real_kernel(const Ctx cx
   mma_epilogue<S, ADJ, NT, false, 0>(cx, tl, B, c0, c1, c2, rhs0, ksplit, sidx, from_f, reinterpret_cast<int *>(As));
 }
 
-// real plans: the 16-byte-copy kernel by default, MHT_MMA_REAL=0 for the
-// fragment-order kernel
-inline bool mma_real16() {
-  const char *e = getenv("MHT_MMA_REAL");
-  return !(e && atoi(e) == 0);
-}
-
-// pipeline variant: MHT_REAL_CFG = 0 (K chunk 32, 2 stages, 4 CTAs/SM) |
-// 1 (32, 3) | 2 (16, 3; c3 forward 6.9 -> 6.1 ms, adjoint 7.7 -> 7.3 ms over 0,
-// profiles/r01_real_cfg_ab.txt) | 3 (16, 4) | 4 (16, 3, 5 CTAs/SM) |
-// 5 (16, 2, 6 CTAs/SM, 80 registers; default: c3 +1.5% over 2 in four
-// back-to-back pairs, profiles/r01_real_occupancy_ab.txt) | 6 (16, 2, 7) |
-// 7 (8, 4, 6)
-inline int real_cfg() {
-  const char *e = getenv("MHT_REAL_CFG");
-  return e ? atoi(e) : 5;
-}
-
-template <bool ADJ, int BKT, int NSTG, int MINB = 4>
-void mma_real_launch_t(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
-  constexpr int smem = rb_smem_bytes<ADJ, BKT, NSTG>();
-  static bool attr = [] {
-    cudaFuncSetAttribute(mma_real_kernel<ADJ, BKT, NSTG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    return true;
-  }();
-  (void)attr;
-  launch_ex(pdl_mma_on(), mma_real_kernel<ADJ, BKT, NSTG, MINB>, dim3((cx.nrhs + 31) / 32, nt), dim3(MM_THREADS), smem,
-            st, cx, tiles, from_f);
-}
+// Real multi-RHS pipeline: K chunk 16 in a 2-stage cp.async ring at 6 CTAs/SM
+// (80 registers): c3 +1.5% over a 3-stage ring at 4 CTAs/SM, and 16 > 32 for
+// the chunk (c3 forward 6.9 -> 6.1 ms; profiles/r01_real_cfg_ab.txt,
+// r01_real_occupancy_ab.txt)
+constexpr int REAL_BK = 16, REAL_NSTG = 2, REAL_MINB = 6;
 
 template <bool ADJ>
 void mma_real_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
-  switch (real_cfg()) {
-    case 1: mma_real_launch_t<ADJ, 32, 3>(cx, tiles, nt, from_f, st); break;
-    case 3: mma_real_launch_t<ADJ, 16, 4>(cx, tiles, nt, from_f, st); break;
-    case 0: mma_real_launch_t<ADJ, 32, 2>(cx, tiles, nt, from_f, st); break;
-    case 4: mma_real_launch_t<ADJ, 16, 3, 5>(cx, tiles, nt, from_f, st); break;
-    case 6: mma_real_launch_t<ADJ, 16, 2, 7>(cx, tiles, nt, from_f, st); break;
-    case 7: mma_real_launch_t<ADJ, 8, 4, 6>(cx, tiles, nt, from_f, st); break;
-    case 2: mma_real_launch_t<ADJ, 16, 3>(cx, tiles, nt, from_f, st); break;
-    default: mma_real_launch_t<ADJ, 16, 2, 6>(cx, tiles, nt, from_f, st);
-  }
+  constexpr int smem = rb_smem_bytes<ADJ, REAL_BK, REAL_NSTG>();
+  auto kern = mma_real_kernel<ADJ, REAL_BK, REAL_NSTG, REAL_MINB>;
+  smem_optin(kern, smem);
+  launch_ex(PDL_MMA, kern, dim3((cx.nrhs + 31) / 32, nt), dim3(MM_THREADS), smem, st, cx, tiles, from_f);
 }
 
-// Multi-RHS configuration (compile-time variants; default picked from the
-// measurements in profiles/, override with MHT_MMA=4m|3m for experiments).
-inline int mma_variant() {
-  static int v = [] {
-    const char *e = getenv("MHT_MMA");
-    if (e && !strcmp(e, "4m")) return 0;   // 4 real MMAs per complex product, 32 RHS per CTA
-    if (e && !strcmp(e, "3m")) return 1;   // 3M, 32 RHS per CTA (3 CTAs/SM)
-    return 1;
-  }();
-  return v;
-}
-
-template <class S, bool ADJ, int NT, bool M3, int MINB>
+// Multi-RHS dispatch: real plans at nrhs >= 32 -> mma_real_kernel; complex
+// plans at nrhs >= 32 -> mma_ws_kernel; narrower widths -> mma_kernel with 8 or
+// 16 right-hand sides per CTA (complex products in Gauss's 3-product form).
+template <class S, bool ADJ, int NT>
 void mma_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
-  launch_ex(pdl_mma_on(), mma_kernel<S, ADJ, NT, M3, MINB>, dim3((cx.nrhs + 8 * NT - 1) / (8 * NT), nt), dim3(MM_THREADS), 0,
+  launch_ex(PDL_MMA, mma_kernel<S, ADJ, NT, true, 4>, dim3((cx.nrhs + 8 * NT - 1) / (8 * NT), nt), dim3(MM_THREADS), 0,
             st, cx, tiles, from_f);
-}
-
-template <class S, bool ADJ, bool M3, int MINB, int NTMAX>
-void mma_launch_nt(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
-  if (NTMAX >= 4 && cx.nrhs >= 32)
-    mma_launch<S, ADJ, 4, M3, MINB>(cx, tiles, nt, from_f, st);
-  else if (cx.nrhs >= 16)
-    mma_launch<S, ADJ, 2, M3, 4>(cx, tiles, nt, from_f, st);
-  else
-    mma_launch<S, ADJ, 1, M3, 4>(cx, tiles, nt, from_f, st);
 }
 
 template <class S, bool ADJ>
 void mma_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += 65535) {
     const int nt = ntiles - t0 < 65535 ? ntiles - t0 : 65535;
-    const int v = Planes<S>::cplx ? mma_variant() : 0;
-    if (!Planes<S>::cplx && cx.nrhs >= 32 && mma_real16()) {
-      mma_real_launch<ADJ>(cx, tiles + t0, nt, from_f, st);
-    } else if (cx.nrhs >= 32 && mma_ws<S, ADJ>()) {
-      if (v >= 1)
-        mma_ws_launch<S, ADJ, true>(cx, tiles + t0, nt, from_f, st);
+    if (cx.nrhs >= 32) {
+      if constexpr (Planes<S>::cplx)
+        mma_ws_launch<ADJ>(cx, tiles + t0, nt, from_f, st);
       else
-        mma_ws_launch<S, ADJ, false>(cx, tiles + t0, nt, from_f, st);
-    } else if (v >= 1)
-      mma_launch_nt<S, ADJ, true, 3, 4>(cx, tiles + t0, nt, from_f, st);
-    else
-      mma_launch_nt<S, ADJ, false, 4, 4>(cx, tiles + t0, nt, from_f, st);
+        mma_real_launch<ADJ>(cx, tiles + t0, nt, from_f, st);
+    } else if (cx.nrhs >= 16) {
+      mma_launch<S, ADJ, 2>(cx, tiles + t0, nt, from_f, st);
+    } else {
+      mma_launch<S, ADJ, 1>(cx, tiles + t0, nt, from_f, st);
+    }
   }
 }
 
@@ -1790,7 +1476,7 @@ __global__ void __launch_bounds__(PERSIST_THREADS, MINB) persist_kernel(const Ct
       if (ph.kind == PH_FWD)
         fwd_tile<S, true>(cx, ftiles[ph.off + t]);
       else if (ph.kind == PH_ADJ)
-        adj_tile<S, 1, true>(cx, atiles[ph.off + t], ph.from_f, 0);
+        adj_tile<S, true>(cx, atiles[ph.off + t], ph.from_f);
       else
         reduce_piece<S, true>(cx, pieces[ph.off + t], rd);
       __syncthreads();
@@ -1813,13 +1499,7 @@ template <class S>
 void fwd_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
     const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
-    const Tile *tp = tiles + t0;
-    if (sizeof(S) == 8 && fwd_fb() == 0)
-      launch_pdl(fwd_kernel<S, 0>, dim3(1, nt), dim3(FWD_THREADS), st, cx, tp);
-    else if (sizeof(S) == 8 && fwd_fb() == 16)
-      launch_pdl(fwd_kernel<S, 16>, dim3(1, nt), dim3(FWD_THREADS), st, cx, tp);
-    else
-      launch_pdl(fwd_kernel<S>, dim3(1, nt), dim3(FWD_THREADS), st, cx, tp);
+    launch_pdl(fwd_kernel<S>, dim3(1, nt), dim3(FWD_THREADS), st, cx, tiles + t0);
   }
 }
 
@@ -1827,15 +1507,7 @@ template <class S>
 void adj_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
     const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
-    const Tile *tp = tiles + t0;
-    if (adj_rch() == 256)
-      launch_pdl(adj_kernel<S, 1, 256>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
-    else if (adj_rch() == 512)
-      launch_pdl(adj_kernel<S, 1, 512>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
-    else if (sizeof(S) == 16 ? adj_ar2() : adj_ar2_real())
-      launch_pdl(adj_kernel<S, 1, ADJ_RCH, true>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
-    else
-      launch_pdl(adj_kernel<S, 1>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tp, from_f);
+    launch_pdl(adj_kernel<S>, dim3(1, nt), dim3(ADJ_THREADS), st, cx, tiles + t0, from_f);
   }
 }
 
@@ -1892,16 +1564,9 @@ void launch_repack(const double *src, double *dst, const Repack *jobs, int njobs
   }
 }
 
-// MINB = CTAs per SM the register budget is sized for: 5 (96 registers; the
-// complex body spills ~200 B outside its loops) or 4 (128, no spills).
-// MHT_PERSIST_MINB=4|5 selects (default 5).
-inline int persist_minb() {
-  static int v = [] {
-    const char *e = getenv("MHT_PERSIST_MINB");
-    return (e && atoi(e) == 4) ? 4 : 5;
-  }();
-  return v;
-}
+// the register budget is sized for 5 CTAs per SM (96 registers; 4 CTAs /
+// 128 registers measured no faster, profiles/r01_persistent_ab.txt)
+constexpr int PERSIST_MINB = 5;
 
 template <class S, int MINB>
 cudaError_t persist_launch(const Ctx &ctx, const Phase *phases, int nph, const Tile *ftiles, const Tile *atiles,
@@ -1919,10 +1584,7 @@ int persist_grid_t() {
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (persist_minb() == 4)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, persist_kernel<S, 4>, PERSIST_THREADS, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, persist_kernel<S, 5>, PERSIST_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, persist_kernel<S, PERSIST_MINB>, PERSIST_THREADS, 0);
   return sms * per;
 }
 
@@ -1932,8 +1594,7 @@ template <class S>
 cudaError_t persist_dispatch(const Ctx &ctx, const Phase *phases, int nph, const Tile *ftiles, const Tile *atiles,
                              const Piece *pieces, const int64_t *rd, int *ctr, unsigned long long *stamps, int grid,
                              cudaStream_t st) {
-  if (persist_minb() == 4) return persist_launch<S, 4>(ctx, phases, nph, ftiles, atiles, pieces, rd, ctr, stamps, grid, st);
-  return persist_launch<S, 5>(ctx, phases, nph, ftiles, atiles, pieces, rd, ctr, stamps, grid, st);
+  return persist_launch<S, PERSIST_MINB>(ctx, phases, nph, ftiles, atiles, pieces, rd, ctr, stamps, grid, st);
 }
 
 int launch_persist(bool is_complex, const Ctx &ctx, const Phase *phases, int nph, const Tile *ftiles,

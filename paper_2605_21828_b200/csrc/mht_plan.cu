@@ -62,7 +62,8 @@ struct Range {
 
 struct mht_plan {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // the stream applies are enqueued on
+  cudaStream_t own_stream = nullptr;  // the plan's own (loader) stream, destroyed with the plan
   bool cplx = false;
   size_t ssz = 8;
   int64_t n = 0, m = 0;
@@ -133,8 +134,7 @@ struct mht_plan {
   std::vector<double> last_phase_ms[2];    // [dir] per-phase durations of the last profiled apply
   bool want_stamps[2] = {false, false};
   int64_t *d_rdtab = nullptr;
-  void *d_tmaps = nullptr;    // CUtensorMap per materialised block (adjoint TMA tiles)
-  void *d_tmaps_f = nullptr;  // ... real forward TMA tiles
+  void *d_tmaps = nullptr;    // CUtensorMap per materialised block (complex adjoint TMA tiles)
   bool fused_sum = true;        // adjoint group sums on the consumer's load (MHT_FUSED_SUM=0: off)
   int n_unfused = 0;
   int64_t n_split_groups = 0;
@@ -151,6 +151,11 @@ struct mht_plan {
   int ws_nrhs = 0;
   void *d_hc = nullptr, *d_hf = nullptr;
   int host_nrhs = 0;
+  // mht_lsqr work vectors (u, v, w, Phi v, Phi^* u, norm partials, per-column
+  // state), kept across calls and grown with nrhs so repeated solves reuse the
+  // same pointers (and the captured graphs keyed on them)
+  void *lsqr_buf[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int lsqr_nrhs = 0;
 
   // profiling: one (start, stop) event pair per recorded launch
   struct Rec {
@@ -165,10 +170,14 @@ struct mht_plan {
   ~mht_plan() {
     if (stream) cudaStreamSynchronize(stream);
     clear_graphs();
+    if (own_stream && own_stream != stream) cudaStreamSynchronize(own_stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (own_stream) cudaStreamDestroy(own_stream);
+    for (void *p : lsqr_buf)
+      if (p) cudaFree(p);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd, (void *)d_fwd1, d_fsplit, (void *)d_fcount,
-                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, (void *)d_phases, (void *)d_ctr, (void *)d_stamps, d_msplit, (void *)d_mcount, d_ctmp, d_tmaps, d_tmaps_f, d_z, d_part, d_hc, d_hf})
+                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, (void *)d_phases, (void *)d_ctr, (void *)d_stamps, d_msplit, (void *)d_mcount, d_ctmp, d_tmaps, d_z, d_part, d_hc, d_hf})
       if (p) cudaFree(p);
   }
 };
@@ -285,7 +294,8 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
   // device coefficient pool: the body size bounds the coefficient bytes.  A
   // shard reads only its own blocks' coefficients (second pass below).
   const bool sharded = sh.G > 1;
-  CUDA_TRY(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&P->own_stream, cudaStreamNonBlocking));
+  P->stream = P->own_stream;
   size_t pool_bytes = std::max<int64_t>(16, body);
   if (!sharded) {
     CUDA_TRY(cudaMalloc(&P->d_coef, pool_bytes));
@@ -647,13 +657,13 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
     P->device_bytes += (int64_t)nbytes;
   }
 
-  // ------------------------------------------------ TMA descriptors (adjoint tiles)
+  // ------------------------------------------------ TMA descriptors (complex adjoint tiles)
   // One 2-D tensor map per block with coefficients: T viewed as a column-major
-  // r_out x n_red array of float64 (complex: 2 r_out doubles per column),
-  // row stride ld; box = BK/2 rows (128 bytes) x 64 columns, 128-byte
-  // swizzle (half of the adjoint tile's K chunk per request), out-of-range
-  // rows / columns zero-filled by the TMA unit.
-  {
+  // (2 r_out doubles) x n_red array of float64, row stride ld; box = 8 complex
+  // rows (128 bytes) x 64 columns, 128-byte swizzle (half of the adjoint
+  // tile's K chunk per request), out-of-range rows / columns zero-filled by
+  // the TMA unit.  Real plans use no tensor maps.
+  if (P->cplx) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
       cudaDriverEntryPointQueryResult q;
@@ -688,29 +698,6 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
     if (!maps.empty())
       CUDA_TRY(cudaMemcpy(P->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     P->device_bytes += (int64_t)maps.size() * (int64_t)sizeof(CUtensorMap);
-    // forward tiles: box = 128-byte rows (16 real / 8 complex) x BK columns,
-    // 128-byte swizzle
-    {
-      std::vector<CUtensorMap> fmaps(blocks.size());
-      for (size_t i = 0; i < blocks.size(); ++i) {
-        const DevBlock &D = blocks[i];
-        memset(&fmaps[i], 0, sizeof(CUtensorMap));
-        if (D.n_red == 0 || D.r_out == 0) continue;
-        cuuint64_t dims[2] = {(cuuint64_t)D.r_out * ew, (cuuint64_t)D.n_red};
-        cuuint64_t strides[1] = {(cuuint64_t)D.ld * P->ssz};
-        cuuint32_t box[2] = {16, (cuuint32_t)bk};
-        cuuint32_t estr[2] = {1, 1};
-        void *addr = static_cast<char *>(P->d_coef) + D.coef_off * (int64_t)P->ssz;
-        CUresult r = encode(&fmaps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, addr, dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(MHT_ERR_CUDA, "cuTensorMapEncodeTiled failed (forward map)");
-      }
-      CUDA_TRY(cudaMalloc(&P->d_tmaps_f, std::max<size_t>(1, fmaps.size()) * sizeof(CUtensorMap)));
-      if (!fmaps.empty())
-        CUDA_TRY(cudaMemcpy(P->d_tmaps_f, fmaps.data(), fmaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-      P->device_bytes += (int64_t)fmaps.size() * (int64_t)sizeof(CUtensorMap);
-    }
   }
 
   // ------------------------------------------------ tiles (LPT order per stage)
@@ -743,13 +730,11 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
   }
   std::vector<Tile> fwd_all, adj_all, adjm_all;
   const int ADJ1_TARGET = prop.multiProcessorCount * 6;
-  int ADJ1_MIN_SPLIT = 128;
-  if (const char *e = getenv("MHT_ASPLIT_MIN")) ADJ1_MIN_SPLIT = std::max(32, atoi(e));
+  const int ADJ1_MIN_SPLIT = 128;
   int64_t asplit_scalars = 0;
   int32_t agroups = 0;
   const int MMA_TARGET = prop.multiProcessorCount * 4;
-  int MMA_MIN_SPLIT = 256;
-  if (const char *e = getenv("MHT_MSPLIT_MIN")) MMA_MIN_SPLIT = std::max(64, atoi(e));
+  const int MMA_MIN_SPLIT = 256;
   int64_t mslabs = 0;
   int32_t mgroups = 0;
   P->fwd.assign(L + 2, Range{});
@@ -845,9 +830,7 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
   // A stage with fewer than FWD1_TARGET row tiles leaves SMs idle; split the
   // columns of its blocks (>= FWD1_MIN_SPLIT columns per split) to reach the target.
   const int FWD1_TARGET = prop.multiProcessorCount * 6;
-  // columns per split: env MHT_SPLIT_MIN (experiments), default 64
-  int FWD1_MIN_SPLIT = 64;
-  if (const char *e = getenv("MHT_SPLIT_MIN")) FWD1_MIN_SPLIT = std::max(32, atoi(e));
+  const int FWD1_MIN_SPLIT = 64;  // columns per split
   std::vector<Tile> fwd1_all;
   P->fwd1.assign(L + 2, Range{});
   int64_t split_scalars = 0;
@@ -1057,7 +1040,6 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
       rdtab.insert(rdtab.end(), rdl[i].begin(), rdl[i].end());
     }
   }
-  if (const char *e = getenv("MHT_FUSED_SUM")) P->fused_sum = strcmp(e, "0") != 0;
 
   // ------------------------------------------------ persistent phases (nrhs = 1)
   {
@@ -1087,7 +1069,6 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
       R.count = (int32_t)P->h_phases.size() - R.off;
     }
   }
-  if (const char *e = getenv("MHT_PERSIST")) P->persist = atoi(e) != 0 ? 1 : 0;
 
   // ------------------------------------------------ upload
   mht_status st;
@@ -1159,11 +1140,6 @@ Ctx make_ctx(mht_plan *P, int nrhs) {
   cx.fcount = P->d_fcount;
   cx.rdtab = P->d_rdtab;
   cx.tmaps = P->d_tmaps;
-  {
-    const char *e = getenv("MHT_WS_B16");
-    cx.b16 = !(e && atoi(e) == 0);
-  }
-  cx.tmaps_f = P->d_tmaps_f;
   cx.diag = P->cur_diag;
   cx.diag_sqrt = P->cur_diag_sqrt;
   cx.msplit = P->d_msplit;
@@ -1476,7 +1452,12 @@ mht_status mht_plan_info_get(const mht_plan *P, mht_plan_info *info) {
 
 mht_status mht_plan_set_stream(mht_plan *P, void *stream) {
   if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
-  // keep our own non-blocking stream for loading; apply on the caller's stream
+  // applies go to the caller's stream; the plan's own stream (used by the
+  // loader, and again after mht_plan_set_stream(P, own)) is kept and
+  // destroyed with the plan.  Work already queued on the previous stream is
+  // ordered before later calls by synchronising it first.
+  CUDA_TRY(cudaSetDevice(P->device));
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
   P->stream = static_cast<cudaStream_t>(stream);
   return MHT_OK;
 }
@@ -1588,22 +1569,25 @@ mht_status mht_lsqr(mht_plan *P, const void *b, void *x, int nrhs, int max_iters
   const size_t sz = P->ssz;
   const int pn = lsqr_partials(n), pm = lsqr_partials(m);
   const int pmax = std::max(pn, pm);
-  struct Buf {
-    void *p = nullptr;
-    ~Buf() {
+  if (nrhs > P->lsqr_nrhs) {
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    P->clear_graphs();  // graphs keyed on the old work vectors
+    for (void *&p : P->lsqr_buf) {
       if (p) cudaFree(p);
+      p = nullptr;
     }
-  } u, v, w, tn, tm, part, col;
-  CUDA_TRY(cudaMalloc(&u.p, (size_t)n * nrhs * sz));
-  CUDA_TRY(cudaMalloc(&v.p, (size_t)m * nrhs * sz));
-  CUDA_TRY(cudaMalloc(&w.p, (size_t)m * nrhs * sz));
-  CUDA_TRY(cudaMalloc(&tn.p, (size_t)n * nrhs * sz));
-  CUDA_TRY(cudaMalloc(&tm.p, (size_t)m * nrhs * sz));
-  CUDA_TRY(cudaMalloc(&part.p, (size_t)pmax * nrhs * sizeof(double)));
-  CUDA_TRY(cudaMalloc(&col.p, (size_t)nrhs * sizeof(LsqrCol)));
-  CUDA_TRY(cudaMemsetAsync(col.p, 0, (size_t)nrhs * sizeof(LsqrCol), P->stream));
-  LsqrCol *dc = static_cast<LsqrCol *>(col.p);
-  double *dp = static_cast<double *>(part.p);
+    P->lsqr_nrhs = 0;
+    const size_t bytes[7] = {(size_t)n * nrhs * sz, (size_t)m * nrhs * sz, (size_t)m * nrhs * sz, (size_t)n * nrhs * sz,
+                             (size_t)m * nrhs * sz, (size_t)pmax * nrhs * sizeof(double), (size_t)nrhs * sizeof(LsqrCol)};
+    for (int i = 0; i < 7; ++i) CUDA_TRY(cudaMalloc(&P->lsqr_buf[i], bytes[i]));
+    P->lsqr_nrhs = nrhs;
+  }
+  struct Buf {
+    void *p;
+  } u{P->lsqr_buf[0]}, v{P->lsqr_buf[1]}, w{P->lsqr_buf[2]}, tn{P->lsqr_buf[3]}, tm{P->lsqr_buf[4]};
+  CUDA_TRY(cudaMemsetAsync(P->lsqr_buf[6], 0, (size_t)nrhs * sizeof(LsqrCol), P->stream));
+  LsqrCol *dc = static_cast<LsqrCol *>(P->lsqr_buf[6]);
+  double *dp = static_cast<double *>(P->lsqr_buf[5]);
   void *s = P->stream;
   const bool cx = P->cplx;
   // beta_1 u_1 = b;  alpha_1 v_1 = Phi^* u_1;  w_1 = v_1;  x_0 = 0

@@ -244,12 +244,23 @@ class Plan:
                                        float(atol), float(btol), C.byref(it), rn, an), "mht_lsqr")
         return x, it.value, np.array(rn[:]), np.array(an[:])
 
+    def _host_out(self, out, nrhs: int, rows: int):
+        """A caller-supplied host output must be exactly what the C side writes:
+        nrhs*rows scalars of the plan's dtype, C-contiguous and writeable (the
+        device-to-host copy cannot check any of this)."""
+        if out is None:
+            return np.empty((nrhs, rows), dtype=self.np_dtype)
+        if not isinstance(out, np.ndarray) or out.dtype != self.np_dtype or not out.flags.c_contiguous \
+                or not out.flags.writeable or out.size != nrhs * rows:
+            raise MhtError(f"host output must be a writeable C-contiguous {np.dtype(self.np_dtype).name} array of "
+                           f"{nrhs} x {rows} entries")
+        return out
+
     def apply_host(self, c_host: np.ndarray, f_host: np.ndarray | None = None):
         """End-to-end call from host memory (pinned for full bandwidth)."""
         c_host = np.ascontiguousarray(c_host, dtype=self.np_dtype).reshape(-1, self.m)
         nrhs = c_host.shape[0]
-        if f_host is None:
-            f_host = np.empty((nrhs, self.n), dtype=self.np_dtype)
+        f_host = self._host_out(f_host, nrhs, self.n)
         self._stream()
         _check(load_library().mht_apply_host(self._h, C.c_void_p(c_host.ctypes.data),
                                              C.c_void_p(f_host.ctypes.data), nrhs), "mht_apply_host")
@@ -258,8 +269,7 @@ class Plan:
     def adjoint_host(self, f_host: np.ndarray, c_host: np.ndarray | None = None):
         f_host = np.ascontiguousarray(f_host, dtype=self.np_dtype).reshape(-1, self.n)
         nrhs = f_host.shape[0]
-        if c_host is None:
-            c_host = np.empty((nrhs, self.m), dtype=self.np_dtype)
+        c_host = self._host_out(c_host, nrhs, self.m)
         self._stream()
         _check(load_library().mht_apply_adjoint_host(self._h, C.c_void_p(f_host.ctypes.data),
                                                      C.c_void_p(c_host.ctypes.data), nrhs),

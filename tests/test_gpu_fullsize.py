@@ -23,6 +23,13 @@ def rel_cols(a, b):
     return max(np.linalg.norm(a[r] - b[r]) / np.linalg.norm(b[r]) for r in range(b.shape[0]))
 
 
+def o2_err(a, b):
+    """Per column, the larger of the relative l2 error and the elementwise
+    max |a - b| / max |b| (every one of the n or m entries is compared)."""
+    assert a.shape == b.shape
+    return max(rel_cols(a, b), max(np.max(np.abs(a[r] - b[r])) / np.max(np.abs(b[r])) for r in range(b.shape[0])))
+
+
 @pytest.fixture(scope="module")
 def gpu():
     if not torch.cuda.is_available():
@@ -46,8 +53,8 @@ def _run(gpu, oracle_lib, w, dense_rows, dense_cols):
         y = mi.workload_adjoint_input(w, nrhs)
         f = P.apply(torch.from_numpy(c).cuda()).cpu().numpy()
         a = P.adjoint(torch.from_numpy(y).cuda()).cpu().numpy()
-        assert rel_cols(f, O.apply(c)) <= 1e-12, ("fwd vs O2", nrhs)
-        assert rel_cols(a, O.adjoint(y)) <= 1e-12, ("adj vs O2", nrhs)
+        assert o2_err(f, O.apply(c)) <= 1e-12, ("fwd vs O2", nrhs)
+        assert o2_err(a, O.adjoint(y)) <= 1e-12, ("adj vs O2", nrhs)
         sub = slice(0, min(nrhs, 4))  # a few columns against the (slow) dense sums
         fd = dense_rows(rows, c[sub])
         assert rel_cols(f[sub][:, rows], fd) <= 10 * w.tol, ("fwd vs dense", nrhs, rel_cols(f[sub][:, rows], fd))
