@@ -1095,8 +1095,9 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
   if ((st = upload(&P->d_phases, P->h_phases, P->device_bytes)) != MHT_OK) return st;
   {
     const int maxph = std::max<int>(1, std::max(P->ph_fwd.count, std::max(P->ph_adj_fused.count, P->ph_adj_unfused.count)));
-    CUDA_TRY(cudaMalloc((void **)&P->d_ctr, (size_t)maxph * sizeof(int)));
-    CUDA_TRY(cudaMemset(P->d_ctr, 0, (size_t)maxph * sizeof(int)));
+    // per-phase done counters + the dequeue and exit counters of the flow kernel
+    CUDA_TRY(cudaMalloc((void **)&P->d_ctr, (size_t)(maxph + 2) * sizeof(int)));
+    CUDA_TRY(cudaMemset(P->d_ctr, 0, (size_t)(maxph + 2) * sizeof(int)));
     CUDA_TRY(cudaMalloc((void **)&P->d_stamps, (size_t)(maxph + 1) * 2 * sizeof(unsigned long long)));
     P->device_bytes += (int64_t)maxph * 4 + (maxph + 1) * 16;
   }

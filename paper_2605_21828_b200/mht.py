@@ -292,8 +292,9 @@ class Plan:
         _check(load_library().mht_set_graphs(self._h, int(bool(on))), "mht_set_graphs")
 
     def set_persistent(self, on: bool):
-        """nrhs = 1 applies as one cooperative launch per direction (True) or
-        one launch per stage (False, default); bitwise identical results."""
+        """nrhs = 1 applies as ONE dataflow launch per direction (True: the
+        flow kernel, TMA-fed, per-phase done counters) or one launch per stage
+        (False).  Both are deterministic; they sum in different orders."""
         _check(load_library().mht_set_persistent(self._h, int(bool(on))), "mht_set_persistent")
 
     def phase_times(self, direction: int):

@@ -319,16 +319,23 @@ def test_split_k_small_blocks(gpu, oracle_lib, plans):
         P.close()
 
 
-def test_persistent_matches_per_stage_launches(gpu, oracle_lib, plans):
-    """nrhs = 1 applies as one cooperative (persistent) launch per direction
-    and as one launch per stage give bitwise-identical results (same tiles,
-    same split order), for complex and real plans with aliases, COPY blocks,
-    split tiles and unfused sums; both match O2; repeated persistent applies
-    (work counters re-armed in-kernel) and graph replay stay identical."""
+def test_flow_kernel_one_launch_apply(gpu, oracle_lib, plans):
+    """nrhs = 1 applies as ONE dataflow launch per direction (mht_set_persistent:
+    TMA ring of factor chunks, per-phase done counters, no grid barrier) on
+    complex and real plans with aliases and COPY blocks, split tiles, unfused
+    sums, wide blocks (x windows reloaded past 1,024 columns) and tall blocks
+    (z windows past 1,024 rows): element-by-element parity with O2 and with the
+    per-stage launches (different summation order: 1e-12, not bitwise),
+    bitwise repeatability across applies (counters re-armed in-kernel) and
+    identical graph replay."""
     rng = np.random.default_rng(21)
     cases = [flat_case(plans, 1024, 32, 4, 1e-15, name="exact"), flat_case(plans, 2048, 32, 4, 1e-8)]
     Phi = rng.standard_normal((3000, 200))
     cases.append((_dense_plan(plans, Phi, 1, 1e-12, "persist_tall"), mi.Workload("pt", "mesh", 3000, 200, "float64", 1e-12, 1)))
+    Phi = rng.standard_normal((200, 3000))
+    cases.append((_dense_plan(plans, Phi, 1, 1e-12, "persist_wide"), mi.Workload("pw", "mesh", 200, 3000, "float64", 1e-12, 1)))
+    path_t, w_t = flat_case(plans, 8192, 16, 2, 1e-10, name="tall")
+    cases.append((path_t, w_t))
     for path, w in cases:
         P = gpu.Plan(path)
         O = oracle_lib.Plan(path)
@@ -337,22 +344,26 @@ def test_persistent_matches_per_stage_launches(gpu, oracle_lib, plans):
         else:
             c, y = mi.real_gaussian(1, w.m, 401), mi.real_gaussian(1, w.n, 402)
         ct, yt = torch.from_numpy(c).cuda(), torch.from_numpy(y).cuda()
+        fo, ao = O.apply(c), O.adjoint(y)
         res = {}
         for mode in (True, False):
             P.set_persistent(mode)
             for fused in (True, False):
                 P.set_fused_sums(fused)
-                f = [P.apply(ct).cpu() for _ in range(3)]
-                a = [P.adjoint(yt).cpu() for _ in range(3)]
-                assert all(torch.equal(f[0], x) for x in f[1:]) and all(torch.equal(a[0], x) for x in a[1:])
-                res[(mode, fused)] = (f[0], a[0])
-        for k in res:
-            assert torch.equal(res[k][0], res[(True, True)][0]), (path, k)
-            assert torch.equal(res[k][1], res[(True, True)][1]), (path, k)
-        assert o2_err(res[(True, True)][0].numpy(), O.apply(c)) <= PARITY
-        assert o2_err(res[(True, True)][1].numpy(), O.adjoint(y)) <= PARITY
-        P.set_persistent(True)
+                for graphs in (True, False):
+                    P.set_graphs(graphs)
+                    f = [P.apply(ct).cpu() for _ in range(3)]
+                    a = [P.adjoint(yt).cpu() for _ in range(3)]
+                    assert all(torch.equal(f[0], x) for x in f[1:]) and all(torch.equal(a[0], x) for x in a[1:])
+                    res[(mode, fused, graphs)] = (f[0], a[0])
+                    assert o2_err(f[0].numpy(), fo) <= PARITY, (path, mode, fused, graphs)
+                    assert o2_err(a[0].numpy(), ao) <= PARITY, (path, mode, fused, graphs)
+        for k in res:  # one summation order per mode: fused / unfused and graphs are bitwise equal
+            assert torch.equal(res[k][0], res[(k[0], True, True)][0]), (path, k)
+            assert torch.equal(res[k][1], res[(k[0], True, True)][1]), (path, k)
+        P.set_persistent(False)
         P.set_fused_sums(True)
+        P.set_graphs(True)
         P.close()
 
 
