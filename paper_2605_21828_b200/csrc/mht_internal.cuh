@@ -109,8 +109,8 @@ constexpr int ADJ_RCH = 1024;    // adjoint rows staged in smem per pass (most b
                                  // 256 / 512 measured 8% slower on c2, profiles/r01_adj_rch_ab.txt)
 constexpr int MMA_COLS = 64;     // redundant columns per multi-RHS adjoint tile
 
-// One phase of the persistent nrhs = 1 apply (a stage's tiles or a list of
-// group-sum pieces), separated from the next by a grid barrier.
+// One phase of the one-launch nrhs = 1 apply (a stage's tiles or a list of
+// group-sum pieces); its units wait for the previous phase's done-counter.
 enum : int32_t { PH_FWD = 0, PH_ADJ = 1, PH_SUM = 2 };
 struct Phase {
   int32_t kind;    // PH_FWD | PH_ADJ | PH_SUM
@@ -120,7 +120,6 @@ struct Phase {
   int32_t stage;   // plan stage (-1: the sums into c)
   int32_t pad;
 };
-constexpr int PERSIST_THREADS = 128;
 
 
 // LSQR per-column state (device resident; mht_lsqr.cu)
@@ -143,17 +142,20 @@ void lsqr_update(bool cplx, void *v, void *w, void *x, int64_t len, int k, const
 void lsqr_xnorm(bool cplx, const void *x, int64_t len, int k, double *partial, LsqrCol *col, void *stream);
 
 // Launchers (mht_kernels.cu).  is_complex selects double2 vs double.
-void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, void *stream);
+// latency: the few-tile variant (x staged per chunk, balanced batches, L2
+// prefetch) instead of the streaming one; the loader picks per stage.
+void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool latency, void *stream);
 void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
                 void *stream);
 // multi-RHS (nrhs >= 2): DMMA kernels; forward uses the 64-row tiles, the
 // adjoint uses 64-column tiles (adjm lists).
 void launch_mma(bool is_complex, bool adjoint, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
                 void *stream);
-// persistent apply: returns a cudaError_t value (0 = launched)
-int launch_persist(bool is_complex, const Ctx &ctx, const Phase *phases, int nph, const Tile *ftiles,
-                   const Tile *atiles, const Piece *pieces, const int64_t *rd, int *ctr, unsigned long long *stamps,
-                   int grid, void *stream);
+// one-launch (dataflow) nrhs = 1 apply of one direction: returns a
+// cudaError_t value (0 = launched).  tiles: the forward (fwd1) or adjoint tile list.
+int launch_persist(bool is_complex, bool adjoint, const Ctx &ctx, const Phase *phases, int nph, const Tile *tiles,
+                   const Piece *pieces, const int64_t *rd, int *ctr, unsigned long long *stamps, int grid,
+                   void *stream);
 int persist_grid(bool is_complex);
 void launch_repack(const double *src, double *dst, const Repack *jobs, int njobs, void *stream);
 void launch_reduce(bool is_complex, const Ctx &ctx, const Piece *pieces, const int64_t *rd,

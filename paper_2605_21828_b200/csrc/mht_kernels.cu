@@ -159,6 +159,184 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
 // ------------------------------------------------------------------------
 // CG: workspace reads through L2 only (the persistent kernel; see in_value)
 template <class S, bool CG>
+__device__ __forceinline__ void fwd_tile_lat(const Ctx &cx, const Tile tl) {
+  using X = Tr<S>;
+  const DevBlock B = cx.blocks[tl.blk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ra = tl.start + lane, rb = tl.start + 32 + lane;
+  const bool va = lane < tl.count, vb = lane + 32 < tl.count;
+  const bool split = tl.pad >= 0;
+  int jbeg = 0, jend = B.n_red;
+  if (split) {
+    const int ks = B.pad;
+    const int chunk = ((B.n_red + ks - 1) / ks + 31) & ~31;
+    jbeg = (tl.pad & 255) * chunk;
+    jend = min(B.n_red, jbeg + chunk);
+  }
+  S acc_a = X::zero(), acc_b = X::zero();
+  const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
+  const int64_t ld = B.ld;
+  // complex: lane owns rows l and l + 32 (one 16-byte load each); real: lane
+  // owns the row pair 2l, 2l + 1 (one 16-byte load; columns are 16-byte
+  // aligned by the loader's repack, the pad row is zero)
+  constexpr bool REAL = sizeof(S) == 8;
+  const bool vp = 2 * lane < tl.count;
+  // x = in[red[j]] for a chunk of up to XCH columns is staged in shared memory
+  // first (one gather round trip for the whole chunk, all threads), so the
+  // factor loads never wait behind an index -> value chain; the warps then
+  // take batches of FB columns in turn (w, w + 4, ...: a tile's tail costs at
+  // most one batch), all of a batch's loads issued before their first use,
+  // with an L2 prefetch of the warp's batch two ahead
+  constexpr int XCH = REAL ? 2048 : 1024;  // 16 KB
+  constexpr int FB = REAL ? 8 : 4;
+  __shared__ S xs[XCH];
+  const bool red_iota = (B.flags & F_RED_IOTA) != 0;
+  const int seg_bytes = tl.count * (int)sizeof(S);  // the tile's rows of one column
+  for (int jc = jbeg; jc < jend; jc += XCH) {
+    const int jn = min(XCH, jend - jc);
+    if (jc > jbeg) __syncthreads();  // every warp is past its reads of the previous chunk
+    for (int j = threadIdx.x; j < jn; j += FWD_THREADS) {
+      const int q = red_iota ? jc + j : cx.idx[B.red_off + jc + j];
+      xs[j] = in_value<S, CG>(cx, B, q, 0);
+    }
+    __syncthreads();
+    const int wb = warp * FB, we = jn;
+    constexpr int JS = 4 * FB;
+    const S *colc = T + (int64_t)jc * ld;
+    for (int j = wb; j < we; j += JS) {
+      {  // L2 prefetch of the batch two ahead: column (lane >> 2), 128-byte lines (lane & 3) (+ 4)
+        const int jp = j + 2 * JS + (lane >> 2);
+        if (jp < we) {
+          const char *pc = reinterpret_cast<const char *>(colc + (int64_t)jp * ld + tl.start);
+          const int o = (lane & 3) * 128;
+          if (o < seg_bytes) prefetch_l2(pc + o);
+          if (o + 512 < seg_bytes) prefetch_l2(pc + o + 512);
+        }
+      }
+      if constexpr (REAL) {
+        double2 t[FB];
+#pragma unroll
+        for (int jj = 0; jj < FB; ++jj)
+          t[jj] = (vp && j + jj < we)
+                      ? Tr<double>::ldT2(reinterpret_cast<const double *>(colc) + (int64_t)(j + jj) * ld + tl.start + 2 * lane)
+                      : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int jj = 0; jj < FB; ++jj) {
+          if (j + jj < we) {
+            const S x = xs[j + jj];
+            X::fma(acc_a, t[jj].x, x);
+            X::fma(acc_b, t[jj].y, x);
+          }
+        }
+      } else {
+        S ta[FB], tb[FB];
+#pragma unroll
+        for (int jj = 0; jj < FB; ++jj) {
+          const bool vj = j + jj < we;
+          const S *cp = colc + (int64_t)(j + jj) * ld;
+          ta[jj] = (va && vj) ? X::ldT(cp + ra) : X::zero();
+          tb[jj] = (vb && vj) ? X::ldT(cp + rb) : X::zero();
+        }
+#pragma unroll
+        for (int jj = 0; jj < FB; ++jj) {
+          if (j + jj < we) {
+            const S x = xs[j + jj];
+            X::fma(acc_a, ta[jj], x);
+            X::fma(acc_b, tb[jj], x);
+          }
+        }
+      }
+    }
+  }
+  __shared__ S red[FWD_THREADS / 32][FWD_ROWS];
+  __shared__ int last;
+  if constexpr (REAL) {
+    red[warp][2 * lane] = acc_a;
+    red[warp][2 * lane + 1] = acc_b;
+  } else {
+    red[warp][lane] = acc_a;
+    red[warp][lane + 32] = acc_b;
+  }
+  __syncthreads();
+  S *scratch = static_cast<S *>(cx.fsplit);
+  const int grp = tl.pad >> 8;
+  if (split) {
+    for (int i = threadIdx.x; i < FWD_ROWS; i += FWD_THREADS) {
+      S sum = red[0][i];
+#pragma unroll
+      for (int w = 1; w < FWD_THREADS / 32; ++w) sum = X::add(sum, red[w][i]);
+      scratch[B.fsp_off + ((int64_t)(tl.start / FWD_ROWS) * B.pad + (tl.pad & 255)) * FWD_ROWS + i] = sum;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(cx.fcount + grp, 1) == B.pad - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+  }
+  for (int i = threadIdx.x; i < FWD_ROWS; i += FWD_THREADS) {
+    if (i >= tl.count) continue;
+    S s;
+    if (split) {
+      s = X::zero();
+      for (int k = 0; k < B.pad; ++k) {
+        const S *p = scratch + B.fsp_off + ((int64_t)(tl.start / FWD_ROWS) * B.pad + k) * FWD_ROWS + i;
+        s = X::add(s, X::ldcg(p));
+      }
+    } else {
+      s = red[0][i];
+#pragma unroll
+      for (int w = 1; w < FWD_THREADS / 32; ++w) s = X::add(s, red[w][i]);
+    }
+    const int row = tl.start + i;
+    if (row < B.n_skel) {
+      const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
+      s = X::add(s, in_value<S, CG>(cx, B, q, 0));
+    }
+    if (B.flags & F_OUT_F)
+      static_cast<S *>(cx.fout)[cx.perm[B.out_off + row]] = s;
+    else
+      static_cast<S *>(cx.z)[B.out_off + row] = s;
+  }
+  if (split && threadIdx.x == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
+}
+
+// nrhs = 1 forward, latency variant (stages with few tiles: c1, c4, the small
+// stages of c2 / c3): x staged per chunk, balanced 4-column batches, L2
+// prefetch two batches ahead, 7 CTAs per SM.  c1 forward 126 -> 108 us, c4 95
+// -> 80 us; on stages of many waves the streaming variant below is faster (c2
+// 6.49 vs 7.52 ms, c3 3.06 vs 3.23 ms; profiles/r02_fwd_variants_ab.txt), so
+// the loader picks per stage by tile count.
+template <class S>
+__global__ void __launch_bounds__(FWD_THREADS, 7) fwd_lat_kernel(const Ctx cx, const Tile *__restrict__ tiles) {
+  const Tile tl = tiles[blockIdx.y];
+  pdl_trigger();
+  {
+    // L2 prefetch of the tile's rows of its first 128 columns (every warp's
+    // first batches)
+    const DevBlock &B = cx.blocks[tl.blk];
+    int jbeg = 0, jend = B.n_red;
+    if (tl.pad >= 0) {
+      const int ks = B.pad;
+      const int chunk = (((B.n_red + ks - 1) / ks) + 31) & ~31;
+      jbeg = (tl.pad & 255) * chunk;
+      jend = min(B.n_red, jbeg + chunk);
+    }
+    const int j = jbeg + threadIdx.x;
+    if (j < jend) {
+      const char *col = reinterpret_cast<const char *>(static_cast<const S *>(cx.coef) + B.coef_off + (int64_t)j * B.ld +
+                                                       tl.start);
+      for (int o = 0; o < tl.count * (int)sizeof(S); o += 128) prefetch_l2(col + o);
+    }
+  }
+  pdl_wait();
+  fwd_tile_lat<S, false>(cx, tl);
+}
+
+// nrhs = 1 forward, streaming variant (stages of many waves): lane j of a
+// warp gathers x for its 32-column group, broadcast by shuffle, 8 columns'
+// loads in flight per step, 72 registers (7 CTAs per SM without the x buffer).
+template <class S, bool CG>
 __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
   using X = Tr<S>;
   const DevBlock B = cx.blocks[tl.blk];
@@ -1440,98 +1618,35 @@ __global__ void __launch_bounds__(256) reduce_kernel(const Ctx cx, const Piece *
 
 
 // ------------------------------------------------------------------------
-// Dataflow nrhs = 1 apply ("flow" kernel): ONE launch walks every phase of a
+// Dataflow nrhs = 1 apply ("flow" kernels): ONE launch walks every phase of a
 // direction (forward: stages 0..L+1; adjoint: the leaf stage, then per stage
 // the unfused group sums and the stage, then the sums into c) with no grid
-// barrier.  The factor bytes (all the HBM traffic at nrhs = 1) never depend
-// on earlier stages, so they are decoupled from the dependency chain:
+// barrier and no per-stage launch, drain or ramp:
 //  * units (the nrhs = 1 tiles and group-sum pieces, phase by phase, LPT
-//    order inside a phase) are dequeued from ONE global counter;
-//  * a PRODUCER warp per CTA streams each unit's factor tile into a ring of
-//    32 KB shared-memory slots with 16-byte cp.async copies (completion on the
-//    slot's mbarrier through cp.async.mbarrier.arrive.noinc), running ahead
-//    across unit and phase boundaries.  1-D TMA bulk copies of one factor
-//    column segment (0.5-1 KB) each reached only 2.6-4.9 TB/s from one
-//    producer warp per SM, 16-byte cp.async 7.1 TB/s
-//    (profiles/r02_tma_stream.txt, tools/tma_stream.cu);
-//  * four CONSUMER warps wait (once per unit) until the previous phase's
-//    done-counter is complete, stage the unit's input vector (x or z) in a
-//    shared window through L2, and reduce the slots from shared memory.
+//    order inside a phase) are dequeued from ONE global counter by resident
+//    128-thread CTAs (7 per SM);
+//  * a CTA first prefetches its unit's factor lines into L2 (the factors never
+//    depend on earlier stages), then waits — once per unit — until the
+//    previous phase's done-counter is complete, then runs the same tile body
+//    as the per-stage kernels (factor streamed by 16-byte register loads,
+//    workspace read through L2), and publishes on its phase's done-counter.
+// The factor stream is register loads from many warps, not a shared-memory
+// ring: a cp.async / TMA ring fed by one producer warp per CTA streamed the
+// strided 1 KB factor-column segments at only 2-4.7 TB/s, register loads from
+// 28 warps per SM at 6.9 TB/s (profiles/r02_tma_stream.txt,
+// r02_ncu_flow_ring_c2.txt).
 // Deadlock freedom: a unit waits only on units of earlier phases, which were
-// dequeued earlier, by CTAs that are resident (they executed the dequeue) and
-// that process their own units in dequeue order — by induction on the unit
-// index every unit completes, whatever the grid size or residency.
-// Counters: done[p] per phase, the dequeue counter (ctr[nph]) and an exit
-// counter (ctr[nph + 1]); the last CTA to exit re-arms all of them.
+// dequeued earlier by CTAs that are resident (they executed the dequeue) and
+// that finish a unit before taking the next — by induction on the unit index
+// every unit completes, whatever the grid size or residency.
+// Counters: done[p] per phase, the dequeue counter ctr[nph] and an exit
+// counter ctr[nph + 1]; the last CTA to exit re-arms all of them.
 // ------------------------------------------------------------------------
-constexpr int FL_CONS = 128;                // consumer threads (4 warps)
-constexpr int FL_THREADS = FL_CONS + 32;    // + one producer warp
-constexpr int FL_SLOT = 32768;              // bytes per ring slot
-constexpr int FL_NS = 3;                    // ring slots per CTA; 2 CTAs per SM (192 KB in flight per SM)
-constexpr int FL_WIN = 512;                 // entries of the x (forward) / z (adjoint) window
-constexpr int FL_ROWS = 64;                 // forward tile rows / adjoint chunk rows (slot row stride)
-constexpr int FL_MAXPH = 32;
-static_assert(FL_WIN >= 4 * FL_ROWS, "the forward cross-warp reduction reuses the window");
+constexpr int FL_THREADS = 128;
+constexpr int FL_MINB = 6;      // CTAs per SM the registers are sized for (<= 80: no spills)
+constexpr int FL_MAXPH = 64;
+constexpr int FL_PF_COLS = 128; // factor columns (forward) / column lines (adjoint) prefetched per unit
 
-template <class S>
-__host__ __device__ constexpr int fl_smem_bytes() {
-  // ring + window (+ pair partner; also the forward cross-warp reduction) + meta + barriers + phase table
-  return FL_NS * FL_SLOT + (FL_WIN + 2) * (int)sizeof(S) + FL_NS * 16 + 2 * FL_NS * 8 +
-         FL_MAXPH * (int)sizeof(Phase) + (FL_MAXPH + 1) * 4 + 64;
-}
-
-struct FlMeta {
-  int unit, k0, kn, flags;  // flags: 1 first chunk of the unit, 2 last chunk
-};
-
-// One unit's chunking, computed identically by the producer and the consumers.
-// forward: k = factor columns [kbeg, kend) of a 64-row tile, chunk = KF columns
-//          (smem [k][64 rows]); adjoint: k = factor rows [kbeg, kend) of an
-//          ACOLS-column tile, chunk = 64 rows (smem [col][64 rows]).
-struct FlUnit {
-  int kind, phase, from_f;
-  Tile tl;
-  int kbeg, kend, nch;
-};
-
-template <class S>
-__device__ __forceinline__ FlUnit fl_unit(const Ctx &cx, const Phase *sph, const int *sstart, int nph, int u,
-                                          const Tile *__restrict__ ftiles, const Tile *__restrict__ atiles) {
-  constexpr int KF = FL_SLOT / (FL_ROWS * (int)sizeof(S));  // forward columns per chunk: 32 complex / 64 real
-  FlUnit U;
-  int p = 0;
-  while (p + 1 < nph && sstart[p + 1] <= u) ++p;
-  const Phase ph = sph[p];
-  U.kind = ph.kind;
-  U.phase = p;
-  U.from_f = ph.from_f;
-  U.tl = Tile{ph.off + (u - sstart[p]), 0, 0, -1};  // PH_SUM: blk = piece index
-  U.kbeg = U.kend = U.nch = 0;
-  if (ph.kind == PH_FWD) {
-    U.tl = ftiles[ph.off + (u - sstart[p])];
-    const DevBlock &B = cx.blocks[U.tl.blk];
-    U.kend = B.n_red;
-    if (U.tl.pad >= 0) {
-      const int chunk = ((B.n_red + B.pad - 1) / B.pad + 31) & ~31;
-      U.kbeg = (U.tl.pad & 255) * chunk;
-      U.kend = min(B.n_red, U.kbeg + chunk);
-    }
-    U.nch = U.kend > U.kbeg ? (U.kend - U.kbeg + KF - 1) / KF : 0;
-  } else if (ph.kind == PH_ADJ) {
-    U.tl = atiles[ph.off + (u - sstart[p])];
-    const DevBlock &B = cx.blocks[U.tl.blk];
-    U.kend = B.r_out;
-    if (U.tl.pad >= 0) {
-      const int chunk = ((B.r_out + B.pad2 - 1) / B.pad2 + 31) & ~31;
-      U.kbeg = (U.tl.pad & 255) * chunk;
-      U.kend = min(B.r_out, U.kbeg + chunk);
-    }
-    U.nch = (U.tl.count > 0 && U.kend > U.kbeg) ? (U.kend - U.kbeg + FL_ROWS - 1) / FL_ROWS : 0;
-  }
-  return U;
-}
-
-__device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(FL_CONS) : "memory"); }
 __device__ __forceinline__ int ld_acquire(const int *p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1543,37 +1658,16 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return ns;
 }
 
-template <class S>
-__global__ void __launch_bounds__(FL_THREADS, 2) flow_kernel(const Ctx cx, const Phase *__restrict__ phases, int nph,
-                                                             const Tile *__restrict__ ftiles,
-                                                             const Tile *__restrict__ atiles,
-                                                             const Piece *__restrict__ pieces,
-                                                             const int64_t *__restrict__ rd, int *ctr,
-                                                             unsigned long long *stamps) {
-  using X = Tr<S>;
-  constexpr bool REAL = sizeof(S) == 8;
-  constexpr int KF = FL_SLOT / (FL_ROWS * (int)sizeof(S));
-  constexpr int ACOLS = adj_cols<S>();
-  constexpr int CPW = ACOLS / 4;  // adjoint columns per consumer warp
-  extern __shared__ __align__(128) unsigned char fl_smem[];
-  unsigned char *ring = fl_smem;
-  S *win = reinterpret_cast<S *>(ring + FL_NS * FL_SLOT);
-  S *red = win;  // forward epilogue only (the window is dead by then)
-  FlMeta *meta = reinterpret_cast<FlMeta *>(win + FL_WIN + 2);
-  uint64_t *full = reinterpret_cast<uint64_t *>(meta + FL_NS);
-  uint64_t *empty = full + FL_NS;
-  Phase *sph = reinterpret_cast<Phase *>(empty + FL_NS);
-  int *sstart = reinterpret_cast<int *>(sph + FL_MAXPH);
-  __shared__ int s_flag;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+template <class S, bool ADJ>
+__global__ void __launch_bounds__(FL_THREADS, FL_MINB) flow_kernel(const Ctx cx, const Phase *__restrict__ phases,
+                                                                   int nph, const Tile *__restrict__ tiles,
+                                                                   const Piece *__restrict__ pieces,
+                                                                   const int64_t *__restrict__ rd, int *ctr,
+                                                                   unsigned long long *stamps) {
+  __shared__ Phase sph[FL_MAXPH];
+  __shared__ int sstart[FL_MAXPH + 1];
+  __shared__ int s_u;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < FL_NS; ++i) {
-      mbar_init(full + i, 64);  // producer: 32 cp.async (noinc) + 32 plain arrivals
-      mbar_init(empty + i, 4); // one arrival per consumer warp
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     int acc = 0;
     for (int p = 0; p < nph; ++p) {
       sph[p] = phases[p];
@@ -1586,300 +1680,85 @@ __global__ void __launch_bounds__(FL_THREADS, 2) flow_kernel(const Ctx cx, const
   __syncthreads();
   const int total = sstart[nph];
   int *done = ctr, *deq = ctr + nph, *exitc = ctr + nph + 1;
-
-  if (warp == 4) {
-    // ------------------------------------------------ producer warp
-    int it = 0;
-    for (;;) {
-      int u = 0;
-      if (lane == 0) u = atomicAdd(deq, 1);
-      u = __shfl_sync(FULL, u, 0);
-      if (u >= total) {
-        const int slot = it % FL_NS;
-        mbar_wait(empty + slot, ((it / FL_NS) & 1) ^ 1);
-        if (lane == 0) meta[slot] = FlMeta{-1, 0, 0, 0};
-        mbar_cp_async_arrive(full + slot);
-        mbar_arrive(full + slot);
-        break;
-      }
-      const FlUnit U = fl_unit<S>(cx, sph, sstart, nph, u, ftiles, atiles);
-      if (U.nch == 0) {  // group-sum piece, COPY block, empty tile: no factor data
-        const int slot = it % FL_NS;
-        mbar_wait(empty + slot, ((it / FL_NS) & 1) ^ 1);
-        if (lane == 0) meta[slot] = FlMeta{u, 0, 0, 3};
-        mbar_cp_async_arrive(full + slot);
-        mbar_arrive(full + slot);
-        ++it;
-        continue;
-      }
-      const DevBlock &B = cx.blocks[U.tl.blk];
-      const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
-      const int64_t ld = B.ld;
-      for (int c = 0; c < U.nch; ++c, ++it) {
-        const int slot = it % FL_NS;
-        mbar_wait(empty + slot, ((it / FL_NS) & 1) ^ 1);
-        unsigned char *dst = ring + slot * FL_SLOT;
-        // 16-byte units: a complex entry, or a real row pair (the real layout has
-        // an even ld and a zero pad row, so an odd segment rounds up into it)
-        constexpr int EPU = 16 / (int)sizeof(S);  // entries per unit
-        const char *Tb = reinterpret_cast<const char *>(T);
-        if (U.kind == PH_FWD) {
-          // column k of the slot: the tile's rows of factor column k0 + k
-          const int k0 = U.kbeg + c * KF, kn = min(KF, U.kend - k0);
-          const int nu = (U.tl.count + EPU - 1) / EPU;
-          if (lane == 0) meta[slot] = FlMeta{u, k0, kn, (c == 0 ? 1 : 0) | (c == U.nch - 1 ? 2 : 0)};
-          for (int j = 0; j < kn; ++j) {
-            const char *src = Tb + ((int64_t)(k0 + j) * ld + U.tl.start) * (int64_t)sizeof(S);
-            for (int r = lane; r < nu; r += 32) cp_async<16>(dst + j * FL_ROWS * sizeof(S) + r * 16, src + r * 16, true);
-          }
-        } else {
-          // column col of the slot: rows k0 .. k0 + kn of factor column tl.start + col
-          const int k0 = U.kbeg + c * FL_ROWS, kn = min(FL_ROWS, U.kend - k0);
-          const int nu = (kn + EPU - 1) / EPU;
-          if (lane == 0) meta[slot] = FlMeta{u, k0, kn, (c == 0 ? 1 : 0) | (c == U.nch - 1 ? 2 : 0)};
-          for (int col = 0; col < U.tl.count; ++col) {
-            const char *src = Tb + ((int64_t)(U.tl.start + col) * ld + k0) * (int64_t)sizeof(S);
-            for (int r = lane; r < nu; r += 32) cp_async<16>(dst + col * FL_ROWS * sizeof(S) + r * 16, src + r * 16, true);
-          }
+  for (;;) {
+    if (threadIdx.x == 0) s_u = atomicAdd(deq, 1);
+    __syncthreads();
+    const int u = s_u;
+    if (u >= total) break;
+    int p = 0;
+    while (p + 1 < nph && sstart[p + 1] <= u) ++p;
+    const Phase ph = sph[p];
+    const int t = ph.off + (u - sstart[p]);
+    if (ph.kind != PH_SUM) {
+      // L2 prefetch of the unit's factor lines while the dependency resolves
+      const Tile tl = tiles[t];
+      const DevBlock &B = cx.blocks[tl.blk];
+      const char *T = reinterpret_cast<const char *>(static_cast<const S *>(cx.coef) + B.coef_off);
+      if (!ADJ) {
+        // forward: the tile's rows of (up to) FL_PF_COLS columns of its range
+        int jbeg = 0, jend = B.n_red;
+        if (tl.pad >= 0) {
+          const int chunk = ((B.n_red + B.pad - 1) / B.pad + 31) & ~31;
+          jbeg = (tl.pad & 255) * chunk;
+          jend = min(B.n_red, jbeg + chunk);
         }
-        mbar_cp_async_arrive(full + slot);  // completes when this lane's copies have landed
-        mbar_arrive(full + slot);           // (lane 0: after its meta store)
-      }
-    }
-    return;
-  }
-
-  // ------------------------------------------------ consumer warps (threads 0..127)
-  const int ctid = threadIdx.x;
-  FlUnit U{};
-  S acc_a = X::zero(), acc_b = X::zero();  // forward: rows (lane, lane + 32) complex / (2 lane, 2 lane + 1) real
-  S acc[CPW];                              // adjoint: the warp's CPW columns
-  S skv = X::zero();                       // forward: this thread's skeleton input (rows ctid < 64)
-  int wb = 0, we = 0;                      // window [wb, we) of the unit's k range
-  for (int it = 0;; ++it) {
-    const int slot = it % FL_NS;
-    mbar_wait(full + slot, (it / FL_NS) & 1);
-    const FlMeta mt = meta[slot];
-    if (mt.unit < 0) break;
-    if (mt.flags & 1) {
-      U = fl_unit<S>(cx, sph, sstart, nph, mt.unit, ftiles, atiles);
-      // the previous phase must be complete (transitively: every earlier one)
-      if (U.phase > 0 && ctid == 0) {
-        const int need = sph[U.phase - 1].count;
-        const int *dp = done + U.phase - 1;
-        if (ld_acquire(dp) < need) {
-          while (ld_acquire(dp) < need) __nanosleep(64);
-        }
-      }
-      cons_sync();
-      acc_a = acc_b = X::zero();
-#pragma unroll
-      for (int v = 0; v < CPW; ++v) acc[v] = X::zero();
-      wb = we = U.kbeg;
-      if (U.kind == PH_FWD && ctid < FL_ROWS) {
-        const DevBlock &B = cx.blocks[U.tl.blk];
-        const int row = U.tl.start + ctid;
-        skv = X::zero();
-        if (ctid < U.tl.count && row < B.n_skel) {
-          const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
-          skv = in_value<S, true>(cx, B, q, 0);
-        }
-      }
-    }
-    const unsigned char *A = ring + slot * FL_SLOT;
-    if (U.kind == PH_SUM) {
-      reduce_piece<S, true>(cx, pieces[U.tl.blk], rd, 0, 1, ctid, FL_CONS);
-    } else if (U.kind == PH_FWD && mt.kn > 0) {
-      const DevBlock &B = cx.blocks[U.tl.blk];
-      if (mt.k0 + mt.kn > we) {  // x window: the next FL_WIN columns of the unit
-        cons_sync();             // every warp is past its reads of the old window
-        wb = mt.k0;
-        we = min(U.kend, wb + FL_WIN);
-        for (int j = ctid; j < we - wb; j += FL_CONS) {
-          const int jj = wb + j;
-          const int q = (B.flags & F_RED_IOTA) ? jj : cx.idx[B.red_off + jj];
-          win[j] = in_value<S, true>(cx, B, q, 0);
-        }
-        cons_sync();
-      }
-      const S *xw = win + (mt.k0 - wb);
-      const S *As = reinterpret_cast<const S *>(A);
-#pragma unroll 4
-      for (int k = warp; k < mt.kn; k += 4) {
-        const S x = xw[k];
-        if constexpr (REAL) {
-          const double2 t = *reinterpret_cast<const double2 *>(As + k * FL_ROWS + 2 * lane);
-          X::fma(acc_a, t.x, x);
-          X::fma(acc_b, t.y, x);
-        } else {
-          X::fma(acc_a, As[k * FL_ROWS + lane], x);
-          X::fma(acc_b, As[k * FL_ROWS + lane + 32], x);
-        }
-      }
-    } else if (U.kind == PH_ADJ && mt.kn > 0) {
-      const DevBlock &B = cx.blocks[U.tl.blk];
-      if (mt.k0 + mt.kn > we) {  // z window: the next FL_WIN rows of the unit
-        cons_sync();
-        wb = mt.k0;
-        we = min(U.kend, wb + FL_WIN);
-        for (int i = ctid; i < we - wb; i += FL_CONS) win[i] = adj_in<S, true>(cx, B, wb + i, 0, U.from_f);
-        if (ctid == 0) win[we - wb] = X::zero();  // pair partner of an odd last row (real)
-        cons_sync();
-      }
-      const S *zw = win + (mt.k0 - wb);
-      const S *As = reinterpret_cast<const S *>(A);
-      const int cbase = warp * CPW;
-      if constexpr (REAL) {
-        const bool ok = 2 * lane < mt.kn;
-        const double z0 = ok ? zw[2 * lane] : 0.0, z1 = ok ? zw[2 * lane + 1] : 0.0;
-#pragma unroll
-        for (int v = 0; v < CPW; ++v) {
-          if (cbase + v < U.tl.count && ok) {
-            const double2 t = *reinterpret_cast<const double2 *>(As + (cbase + v) * FL_ROWS + 2 * lane);
-            double &a = reinterpret_cast<double &>(acc[v]);
-            a = ::fma(t.x, z0, a);
-            a = ::fma(t.y, z1, a);
-          }
+        const int j = jbeg + threadIdx.x;
+        if (j < jend && threadIdx.x < FL_PF_COLS) {
+          const char *col = T + ((int64_t)j * B.ld + tl.start) * (int64_t)sizeof(S);
+          for (int o = 0; o < tl.count * (int)sizeof(S); o += 128) prefetch_l2(col + o);
         }
       } else {
-        const bool oka = lane < mt.kn, okb = lane + 32 < mt.kn;
-        const S z0 = oka ? zw[lane] : X::zero(), z1 = okb ? zw[lane + 32] : X::zero();
-#pragma unroll
-        for (int v = 0; v < CPW; ++v) {
-          if (cbase + v < U.tl.count) {
-            if (oka) X::fmac(acc[v], As[(cbase + v) * FL_ROWS + lane], z0);
-            if (okb) X::fmac(acc[v], As[(cbase + v) * FL_ROWS + lane + 32], z1);
-          }
-        }
+        // adjoint: the first 1 KB of each of the tile's columns (rows of its range)
+        int rbeg = 0;
+        if (tl.pad >= 0) rbeg = (tl.pad & 255) * ((((B.r_out + B.pad2 - 1) / B.pad2) + 31) & ~31);
+        const int col = tl.start + (threadIdx.x >> 3), line = threadIdx.x & 7;
+        if ((threadIdx.x >> 3) < tl.count && line * 128 < (B.r_out - rbeg) * (int)sizeof(S))
+          prefetch_l2(T + ((int64_t)col * B.ld + rbeg) * (int64_t)sizeof(S) + line * 128);
       }
     }
-    // release the slot (every lane of the warp is past its reads)
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + slot);
-    if (!(mt.flags & 2)) continue;
-
-    // ---------------------------------------------- unit epilogue
-    if (U.kind == PH_FWD) {
-      const DevBlock &B = cx.blocks[U.tl.blk];
-      const bool split = U.tl.pad >= 0;
-      cons_sync();  // every warp is past its window reads (red aliases the window)
-      if constexpr (REAL) {
-        red[warp * FL_ROWS + 2 * lane] = acc_a;
-        red[warp * FL_ROWS + 2 * lane + 1] = acc_b;
-      } else {
-        red[warp * FL_ROWS + lane] = acc_a;
-        red[warp * FL_ROWS + lane + 32] = acc_b;
-      }
-      cons_sync();
-      S *scratch = static_cast<S *>(cx.fsplit);
-      const int grp = U.tl.pad >> 8;
-      bool last = true;
-      if (split) {
-        if (ctid < FL_ROWS) {
-          const S sum = X::add(X::add(red[ctid], red[FL_ROWS + ctid]), X::add(red[2 * FL_ROWS + ctid], red[3 * FL_ROWS + ctid]));
-          scratch[B.fsp_off + ((int64_t)(U.tl.start / FWD_ROWS) * B.pad + (U.tl.pad & 255)) * FWD_ROWS + ctid] = sum;
-        }
-        __threadfence();
-        cons_sync();
-        if (ctid == 0) s_flag = atomicAdd(cx.fcount + grp, 1) == B.pad - 1;
-        cons_sync();
-        last = s_flag != 0;
-        if (last) __threadfence();
-      }
-      if (last && ctid < U.tl.count) {
-        S s;
-        if (split) {
-          s = X::zero();
-          for (int k = 0; k < B.pad; ++k)
-            s = X::add(s, X::ldcg(scratch + B.fsp_off + ((int64_t)(U.tl.start / FWD_ROWS) * B.pad + k) * FWD_ROWS + ctid));
-        } else {
-          s = X::add(X::add(red[ctid], red[FL_ROWS + ctid]), X::add(red[2 * FL_ROWS + ctid], red[3 * FL_ROWS + ctid]));
-        }
-        const int row = U.tl.start + ctid;
-        if (row < B.n_skel) s = X::add(s, skv);
-        if (B.flags & F_OUT_F)
-          static_cast<S *>(cx.fout)[cx.perm[B.out_off + row]] = s;
-        else
-          static_cast<S *>(cx.z)[B.out_off + row] = s;
-      }
-      if (split && last && ctid == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
-    } else if (U.kind == PH_ADJ) {
-      const DevBlock &B = cx.blocks[U.tl.blk];
-      const bool split = U.tl.pad >= 0;
-      const int sidx = split ? (U.tl.pad & 255) : 0;
-      // skeleton part w[skel[i]] = z[i]: the block's first tile
-      if (U.tl.start == 0 && sidx == 0 && B.n_skel > 0) {
-        for (int i = ctid; i < B.n_skel; i += FL_CONS) {
-          const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
-          static_cast<S *>(cx.part)[B.part_off + q] = adj_in<S, true>(cx, B, i, 0, U.from_f);
-        }
-      }
-#pragma unroll
-      for (int v = 0; v < CPW; ++v)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc[v] = X::add(acc[v], X::shfl_xor(acc[v], o));
-      const int cbase = U.tl.start + warp * CPW, cend = U.tl.start + U.tl.count;
-      if (!split) {
-        if (lane == 0) {
-#pragma unroll
-          for (int v = 0; v < CPW; ++v) {
-            const int col = cbase + v;
-            if (col >= cend) continue;
-            const int q = (B.flags & F_RED_IOTA) ? col : cx.idx[B.red_off + col];
-            static_cast<S *>(cx.part)[B.part_off + q] = acc[v];
-          }
-        }
-      } else {
-        S *scratch = static_cast<S *>(cx.fsplit);
-        const int grp = U.tl.pad >> 8;
-        const int64_t sbase = B.asp_off + (int64_t)(U.tl.start / ACOLS) * B.pad2 * ACOLS;
-        if (lane == 0) {
-#pragma unroll
-          for (int v = 0; v < CPW; ++v) scratch[sbase + (int64_t)sidx * ACOLS + warp * CPW + v] = acc[v];
-        }
-        __threadfence();
-        cons_sync();
-        if (ctid == 0) s_flag = atomicAdd(cx.fcount + grp, 1) == B.pad2 - 1;
-        cons_sync();
-        if (s_flag) {
-          __threadfence();
-          for (int c = ctid; c < U.tl.count; c += FL_CONS) {
-            S sum = X::zero();
-            for (int k = 0; k < B.pad2; ++k) sum = X::add(sum, X::ldcg(scratch + sbase + (int64_t)k * ACOLS + c));
-            const int col = U.tl.start + c;
-            const int q = (B.flags & F_RED_IOTA) ? col : cx.idx[B.red_off + col];
-            static_cast<S *>(cx.part)[B.part_off + q] = sum;
-          }
-          if (ctid == 0) cx.fcount[grp] = 0;
-        }
-      }
+    // the previous phase must be complete (transitively: every earlier one)
+    if (p > 0 && threadIdx.x == 0) {
+      const int need = sph[p - 1].count;
+      const int *dp = done + p - 1;
+      while (ld_acquire(dp) < need) __nanosleep(200);
     }
-    // unit complete: publish (release) on the phase's done counter
-    __threadfence();
-    cons_sync();
-    if (ctid == 0) {
-      const int old = atomicAdd(done + U.phase, 1);
-      if (stamps && old == sph[U.phase].count - 1) stamps[U.phase + 1] = globaltimer();
+    __syncthreads();
+    if (ph.kind == PH_SUM)
+      reduce_piece<S, true>(cx, pieces[t], rd, 0, 1, threadIdx.x, FL_THREADS);
+    else if (!ADJ)
+      fwd_tile_lat<S, true>(cx, tiles[t]);
+    else
+      adj_tile<S, true>(cx, tiles[t], ph.from_f);
+    // unit complete: publish on the phase's done counter (the barrier orders
+    // every thread's stores before thread 0's fence; the fence is cumulative)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const int old = atomicAdd(done + p, 1);
+      if (stamps && old == ph.count - 1) stamps[p + 1] = globaltimer();
     }
   }
-  // every unit of this CTA is done and its producer has dequeued for the last
-  // time: the last CTA out re-arms the counters for the next apply
-  cons_sync();
-  if (ctid == 0) {
+  // this CTA has dequeued for the last time and finished its units: the last
+  // CTA out re-arms the counters for the next apply
+  if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(exitc, 1) == (int)gridDim.x - 1) {
-      for (int p = 0; p < nph + 2; ++p) ctr[p] = 0;
+      for (int q = 0; q < nph + 2; ++q) ctr[q] = 0;
       __threadfence();
     }
   }
 }
+
 constexpr int MAX_GRID_Y = 65535;
 
 template <class S>
-void fwd_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, cudaStream_t st) {
+void fwd_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, bool latency, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
     const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
-    launch_pdl(fwd_kernel<S>, dim3(1, nt), dim3(FWD_THREADS), st, cx, tiles + t0);
+    if (latency)
+      launch_pdl(fwd_lat_kernel<S>, dim3(1, nt), dim3(FWD_THREADS), st, cx, tiles + t0);
+    else
+      launch_pdl(fwd_kernel<S>, dim3(1, nt), dim3(FWD_THREADS), st, cx, tiles + t0);
   }
 }
 
@@ -1893,12 +1772,12 @@ void adj_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cuda
 
 }  // namespace
 
-void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, void *stream) {
+void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool latency, void *stream) {
   if (ntiles <= 0) return;
   if (is_complex)
-    fwd_dispatch<double2>(ctx, tiles, ntiles, (cudaStream_t)stream);
+    fwd_dispatch<double2>(ctx, tiles, ntiles, latency, (cudaStream_t)stream);
   else
-    fwd_dispatch<double>(ctx, tiles, ntiles, (cudaStream_t)stream);
+    fwd_dispatch<double>(ctx, tiles, ntiles, latency, (cudaStream_t)stream);
 }
 
 void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
@@ -1946,30 +1825,32 @@ void launch_repack(const double *src, double *dst, const Repack *jobs, int njobs
 
 template <class S>
 int flow_grid_t() {
-  int dev = 0, sms = 0, per = 0;
+  int dev = 0, sms = 0, pf = 0, pa = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  smem_optin<flow_kernel<S>>(fl_smem_bytes<S>());
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, flow_kernel<S>, FL_THREADS, fl_smem_bytes<S>());
-  return sms * per;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, flow_kernel<S, false>, FL_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pa, flow_kernel<S, true>, FL_THREADS, 0);
+  return sms * (pf < pa ? pf : pa);
 }
 
 int persist_grid(bool is_complex) { return is_complex ? flow_grid_t<double2>() : flow_grid_t<double>(); }
 
-int launch_persist(bool is_complex, const Ctx &ctx, const Phase *phases, int nph, const Tile *ftiles,
-                   const Tile *atiles, const Piece *pieces, const int64_t *rd, int *ctr, unsigned long long *stamps,
-                   int grid, void *stream) {
+int launch_persist(bool is_complex, bool adjoint, const Ctx &ctx, const Phase *phases, int nph, const Tile *tiles,
+                   const Piece *pieces, const int64_t *rd, int *ctr, unsigned long long *stamps, int grid,
+                   void *stream) {
   if (nph <= 0) return 0;
   if (nph > FL_MAXPH) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
   if (is_complex) {
-    smem_optin<flow_kernel<double2>>(fl_smem_bytes<double2>());
-    flow_kernel<double2><<<grid, FL_THREADS, fl_smem_bytes<double2>(), st>>>(ctx, phases, nph, ftiles, atiles, pieces,
-                                                                               rd, ctr, stamps);
+    if (adjoint)
+      flow_kernel<double2, true><<<grid, FL_THREADS, 0, st>>>(ctx, phases, nph, tiles, pieces, rd, ctr, stamps);
+    else
+      flow_kernel<double2, false><<<grid, FL_THREADS, 0, st>>>(ctx, phases, nph, tiles, pieces, rd, ctr, stamps);
   } else {
-    smem_optin<flow_kernel<double>>(fl_smem_bytes<double>());
-    flow_kernel<double><<<grid, FL_THREADS, fl_smem_bytes<double>(), st>>>(ctx, phases, nph, ftiles, atiles, pieces, rd,
-                                                                           ctr, stamps);
+    if (adjoint)
+      flow_kernel<double, true><<<grid, FL_THREADS, 0, st>>>(ctx, phases, nph, tiles, pieces, rd, ctr, stamps);
+    else
+      flow_kernel<double, false><<<grid, FL_THREADS, 0, st>>>(ctx, phases, nph, tiles, pieces, rd, ctr, stamps);
   }
   return (int)cudaGetLastError();
 }

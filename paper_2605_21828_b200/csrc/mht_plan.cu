@@ -115,6 +115,9 @@ struct mht_plan {
   int64_t *d_rd = nullptr;
 
   std::vector<Range> fwd, fwd1, adj, adjm, pieces;  // per stage 0..L+1
+  // nrhs = 1 forward variant per stage: 1 = latency (fewer than two waves of
+  // tiles at 7 CTAs per SM), 0 = streaming
+  std::vector<char> fwd1_lat;
   std::vector<Range> pieces_u;  // pieces of the producers that are not fused (fused mode)
   // sharded plans (mht_plan_load_shard): G ranks, this is rank g, switch level ls;
   // exchange layout in zpool entries (x nrhs scalars each)
@@ -873,6 +876,8 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
     P->fwd1[s] = Range{(int32_t)fwd1_all.size(), (int32_t)lst.size()};
     for (auto &x : lst) fwd1_all.push_back(x.second);
   }
+  P->fwd1_lat.assign(L + 2, 0);
+  for (int s = 0; s < L + 2; ++s) P->fwd1_lat[s] = P->fwd1[s].count < 2 * 7 * prop.multiProcessorCount ? 1 : 0;
   P->n_split_groups = groups;
   P->m_slabs = mslabs;
   P->m_groups = mgroups;
@@ -1196,8 +1201,8 @@ unsigned long long *stamp_buf(mht_plan *P, int dir) {
 mht_status run_persist(mht_plan *P, const Ctx &cx, Range ph, int dir) {
   int err = 0;
   timed(P, dir, -2, 1, 1, [&] {
-    err = launch_persist(P->cplx, cx, P->d_phases + ph.off, ph.count, P->d_fwd1, P->d_adj, P->d_pieces, P->d_rd,
-                         P->d_ctr, stamp_buf(P, dir), P->persist_grid, P->stream);
+    err = launch_persist(P->cplx, dir == 1, cx, P->d_phases + ph.off, ph.count, dir == 1 ? P->d_adj : P->d_fwd1,
+                         P->d_pieces, P->d_rd, P->d_ctr, stamp_buf(P, dir), P->persist_grid, P->stream);
   });
   if (err != 0) return fail(MHT_ERR_CUDA, std::string("persistent launch: ") + cudaGetErrorString((cudaError_t)err));
   return MHT_OK;
@@ -1219,7 +1224,7 @@ mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs, int part =
   for (int s = s_lo; s <= s_hi; ++s)
     timed(P, 0, s, nrhs, nrhs == 1 ? P->fwd1[s].count : P->fwd[s].count, [&] {
       if (nrhs == 1)
-        launch_fwd(P->cplx, cx, P->d_fwd1 + P->fwd1[s].off, P->fwd1[s].count, P->stream);
+        launch_fwd(P->cplx, cx, P->d_fwd1 + P->fwd1[s].off, P->fwd1[s].count, P->fwd1_lat[s] != 0, P->stream);
       else
         launch_mma(P->cplx, false, cx, P->d_fwd + P->fwd[s].off, P->fwd[s].count, false, P->stream);
     });

@@ -18,7 +18,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 w = mi.WORKLOADS[name]
 path = W.plan_cache_path(w)
 if not os.path.exists(path):
-    W.build_workload_plan(w, path + ".build", builder="gpu", log=None)
+    W.build_workload_plan(w, path + ".build", builder="gpu" if os.environ.get("CUDA_VISIBLE_DEVICES", "x") != "" else "cpu", log=None)
     os.replace(path + ".build", path)
 pv = PlanView(path)
 print(f"# {name}: n={pv.n} m={pv.m} L={pv.L} complex={pv.complex} entries={pv.entries}")
