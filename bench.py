@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--impl", default="mht", choices=["mht", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(mi.WORKLOADS))
     ap.add_argument("--builder", default="gpu", choices=["gpu", "cpu"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -415,7 +415,7 @@ def main():
         alg = (8 if P.is_complex else 2) * entries * dr / (dn / args.steps)
         achieved = alg / (per_launch_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["dmma_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["dmma_tflops"],
+                "frac": achieved / peaks["dmma_tflops"], "frac_of_burst_peak": achieved / peaks["dmma_tflops_burst"],
                 "frac_of_nominal": achieved / (148 * 64 * 2 * 1.965e9 / 1e12),  # 37.2 TF: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz
                 "traffic": traffic, "algorithmic_flops_per_launch": alg,
                 "kernel": (f"{'mma_ws_kernel' if P.is_complex else 'mma_real_kernel'} {dkind} nrhs={dr} "
@@ -425,6 +425,9 @@ def main():
         if P.is_complex:
             roof["note"] = ("achieved counts 8 real flops per complex multiply-add (algorithmic); the kernel "
                             "issues 3 real DMMA products per complex product (Gauss), so pipe work is 3/4 of that")
+            roof["pipe_frac"] = 0.75 * achieved / peaks["dmma_tflops"]  # issued DMMA work / the pipe's peak
+        else:
+            roof["pipe_frac"] = achieved / peaks["dmma_tflops"]
     if traffic is not None:
         roof["traffic_source"] = _traffic_src(w.name)
     roof["per_launch_ms"] = per_launch_ms
@@ -451,7 +454,7 @@ def main():
 
     # ---- end to end through the C ABI with pinned host buffers
     if not args.no_e2e:
-        out["e2e"] = _e2e(P, phases, w, ws, args)
+        out["e2e"] = _e2e(P, phases, w, ws, args, device_ms_per_step=total_ms / args.steps)
     # ---- CPU oracle baseline (rank 0, N = 1)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         v, reps, el, cores = time_oracle(path, w, args.cpu_seconds)
@@ -531,13 +534,19 @@ def run_shard(args, w, path, ws, rank, lrank):
     dist.destroy_process_group()
 
 
-def _e2e(P, phases, w, ws, args):
+def _e2e(P, phases, w, ws, args, device_ms_per_step=None):
+    """The same step through the C ABI's host-buffer calls (mht_apply_host /
+    mht_apply_adjoint_host): every phase copies its input from pinned host
+    memory, replays the apply and copies the result back, inside the timed
+    region.  Also measures the host<->device link on this box (pinned torch
+    copies of the widest phase's vectors, CUDA events, each direction alone)
+    so the e2e time can be checked against device time + bytes / link rate."""
     import torch
 
     host_in, host_out = {}, {}
     h2d = d2h = 0
     for kind, r in phases:
-        nin, nout = (w.m, w.n) if kind == "fwd" else (w.n, w.m)
+        nout = w.n if kind == "fwd" else w.m
         src = (mi.workload_coefficients(w, r) if kind == "fwd" else mi.workload_adjoint_input(w, r))
         ti = torch.from_numpy(src).pin_memory()
         to = torch.empty((r, nout), dtype=P.torch_dtype).pin_memory()
@@ -559,14 +568,41 @@ def _e2e(P, phases, w, ws, args):
     step()
     step()
     barrier(ws)
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         step()
     el = allreduce_max(time.perf_counter() - t0, ws)
+    clk = clocks.stop()
     transforms = sum(r for _, r in phases)
-    return {"value": ws * transforms * args.e2e_steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-            "api": "mht_apply_host / mht_apply_adjoint_host (pinned host buffers, copies in the timed region)"}
+    # link rates on this box: the widest phase's input (H2D) and output (D2H)
+    big_in = max(host_in.values(), key=lambda t: t.numel())
+    big_out = max(host_out.values(), key=lambda t: t.numel())
+    dev_in = torch.empty_like(big_in, device="cuda")
+    dev_out = torch.empty_like(big_out, device="cuda")
+    rates = {}
+    for name, dst, src_ in (("h2d", dev_in, big_in), ("d2h", big_out, dev_out)):
+        best = None
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            dst.copy_(src_, non_blocking=True)
+            b.record()
+            torch.cuda.synchronize()
+            t = a.elapsed_time(b)
+            best = t if best is None else min(best, t)
+        rates[name] = src_.numel() * P.scalar_bytes / (best / 1e3) / 1e9
+    out = {"value": ws * transforms * args.e2e_steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "ms_per_step": 1e3 * el / args.e2e_steps,
+           "link_GBps": {"h2d": rates["h2d"], "d2h": rates["d2h"],
+                         "how": "pinned torch copy of the widest phase's vector, best of 5, CUDA events"},
+           "clocks": clk,
+           "api": "mht_apply_host / mht_apply_adjoint_host (pinned host buffers, copies in the timed region)"}
+    if device_ms_per_step is not None:
+        out["copy_floor_ms_per_step"] = 1e3 * (h2d / (rates["h2d"] * 1e9) + d2h / (rates["d2h"] * 1e9))
+        out["device_ms_per_step"] = device_ms_per_step
+    return out
 
 
 def _peaks():
@@ -584,15 +620,23 @@ def _peaks():
         out["hbm_gbs"] = 6650.0
         out["hbm_src"] = "fallback (B200_PROFILING.md 6.65 TB/s)"
         smax = 1965.0
-    fp = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    cands = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("fp64_peak.json"))
+    fp = os.path.join(ROOT, "profiles", cands[-1]) if cands else ""
     try:
         d = json.load(open(fp))
-        out["fp64_tflops"] = float(d["dfma_tflops"])
-        out["dmma_tflops"] = float(d["dmma_m16n8k4_tflops"])
+        # the kernels are timed inside long steps: the sustained figure (the
+        # burst one is reported beside it)
+        sus = "dmma_m16n8k4_tflops_sustained" in d
+        out["fp64_tflops"] = float(d["dfma_tflops_sustained" if sus else "dfma_tflops"])
+        out["dmma_tflops"] = float(d["dmma_m16n8k4_tflops_sustained" if sus else "dmma_m16n8k4_tflops"])
+        out["dmma_tflops_burst"] = float(d["dmma_m16n8k4_tflops"])
+        clk = d.get("clocks", {})
         out["fp64_src"] = f"measured DFMA microbenchmark ({os.path.relpath(fp, ROOT)})"
-        out["dmma_src"] = f"measured DMMA m16n8k4 microbenchmark ({os.path.relpath(fp, ROOT)})"
+        out["dmma_src"] = (f"measured DMMA m16n8k4 microbenchmark, {'sustained 3 s' if sus else 'burst'} "
+                           f"({os.path.relpath(fp, ROOT)}; SM clock median {clk.get('sm_mhz')} MHz, "
+                           f"reasons {clk.get('reasons')})")
     except Exception:
-        out["fp64_tflops"] = out["dmma_tflops"] = 148 * 64 * 2 * smax * 1e6 / 1e12
+        out["fp64_tflops"] = out["dmma_tflops"] = out["dmma_tflops_burst"] = 148 * 64 * 2 * smax * 1e6 / 1e12
         out["fp64_src"] = out["dmma_src"] = "derived: 148 SMs x 64 FP64 FMA/clk x 2 x sm_max_mhz"
     return out
 

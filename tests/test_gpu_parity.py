@@ -521,3 +521,35 @@ def test_multi_rhs_kernels_repeatable(gpu, oracle_lib, plans, family):
         assert o2_err(f0.cpu().numpy(), O.apply(c)) <= PARITY
         assert o2_err(a0.cpu().numpy(), O.adjoint(y)) <= PARITY
     P.close()
+
+
+def test_multi_rhs_stress_repeatable(gpu, oracle_lib, plans):
+    """Race stress for the multi-RHS pipelines (compute-sanitizer is closed on
+    this pool, profiles/r02_sanitizer_closed.txt): 60 back-to-back synthesis +
+    analysis pairs per width on a complex plan (warp-specialised TMA / mbarrier
+    kernel at nrhs >= 32, including a partial second RHS chunk, and the K-split
+    slabs of tall blocks) and a real plan (cp.async ring kernel), graphs on, no
+    synchronisation between applies; every result is bitwise identical to the
+    first, which matches O2 element by element."""
+    cases = [flat_case(plans, 8192, 16, 2, 1e-10, name="tall"), flat_case(plans, 2048, 32, 4, 1e-8)]
+    sp = str(plans / "sph_stress.plan")
+    ws = W.sphere_workload(2048, 31, 4, 1e-10)
+    W.build_workload_plan(ws, sp, workers=8, log=None)
+    cases.append((sp, ws))
+    for path, w in cases:
+        P = gpu.Plan(path)
+        O = oracle_lib.Plan(path)
+        gen = mi.real_gaussian if w.dtype == "float64" else mi.complex_gaussian
+        for nrhs in (32, 48, 64):
+            c, y = gen(nrhs, w.m, 1400 + nrhs), gen(nrhs, w.n, 1500 + nrhs)
+            ct, yt = torch.from_numpy(c).cuda(), torch.from_numpy(y).cuda()
+            f0, a0 = P.apply(ct).clone(), P.adjoint(yt).clone()
+            fs, as_ = [], []
+            for _ in range(60):
+                fs.append(P.apply(ct).clone())
+                as_.append(P.adjoint(yt).clone())
+            torch.cuda.synchronize()
+            assert all(torch.equal(f0, x) for x in fs) and all(torch.equal(a0, x) for x in as_), (path, nrhs)
+            assert o2_err(f0.cpu().numpy(), O.apply(c)) <= PARITY
+            assert o2_err(a0.cpu().numpy(), O.adjoint(y)) <= PARITY
+        P.close()

@@ -2,6 +2,7 @@
 // DFMA: independent FMA chains per thread; DMMA: mma.sync.m16n8k4 f64 (and m8n8k4).
 // Prints JSON with TFLOP/s (2 flops per FMA).
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 template <int CH>
@@ -58,44 +59,53 @@ __global__ void dmma_k16_kernel(double *out, int iters) {
   if (s == 123.456) out[threadIdx.x] = s;
 }
 
-int main() {
+// time `launch` once (burst) and back to back for `secs` seconds (sustained);
+// returns {burst ms, sustained ms per launch}
+template <class F>
+static void time_it(F launch, double secs, float &burst, float &sustained) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  launch();  // warm-up
+  cudaEventRecord(e0);
+  launch();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&burst, e0, e1);
+  const int reps = secs > 0 ? (int)(secs * 1e3 / burst) + 1 : 1;
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) launch();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float tot = 0;
+  cudaEventElapsedTime(&tot, e0, e1);
+  sustained = tot / reps;
+}
+
+int main(int argc, char **argv) {
+  const double secs = argc > 1 ? atof(argv[1]) : 0.0;  // sustained window per kernel
   double *d;
   cudaMalloc(&d, 1 << 20);
   cudaDeviceProp p;
   cudaGetDeviceProperties(&p, 0);
   int sms = p.multiProcessorCount;
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  float ms;
-  // DFMA: 8 chains, 256 threads, 4 CTAs/SM
-  int iters = 20000;
+  const int iters = 20000;
   dim3 grid(sms * 8), blk(256);
-  dfma_kernel<8><<<grid, blk>>>(d, 100, 1.0000001, 1e-9);
-  cudaEventRecord(e0);
-  dfma_kernel<8><<<grid, blk>>>(d, iters, 1.0000001, 1e-9);
-  cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
-  cudaEventElapsedTime(&ms, e0, e1);
-  double dfma = 2.0 * 8 * iters * (double)grid.x * blk.x / (ms * 1e-3) / 1e12;
-  // DMMA m16n8k4: 512 FMA per warp-instr, 4 independent accumulators
-  int it2 = 20000;
-  dmma_k4_kernel<<<grid, blk>>>(d, 100);
-  cudaEventRecord(e0);
-  dmma_k4_kernel<<<grid, blk>>>(d, it2);
-  cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
-  cudaEventElapsedTime(&ms, e0, e1);
-  double dmma4 = 2.0 * 512 * 4 * it2 * (double)grid.x * (blk.x / 32) / (ms * 1e-3) / 1e12;
-  dmma_k16_kernel<<<grid, blk>>>(d, 100);
-  cudaEventRecord(e0);
-  dmma_k16_kernel<<<grid, blk>>>(d, it2);
-  cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
-  cudaEventElapsedTime(&ms, e0, e1);
-  double dmma16 = 2.0 * 2048 * 2 * it2 * (double)grid.x * (blk.x / 32) / (ms * 1e-3) / 1e12;
+  float b1, s1, b2, s2, b3, s3;
+  // DFMA: 8 chains, 256 threads, 8 CTAs/SM
+  time_it([&] { dfma_kernel<8><<<grid, blk>>>(d, iters, 1.0000001, 1e-9); }, secs, b1, s1);
+  const double fl_dfma = 2.0 * 8 * iters * (double)grid.x * blk.x;
+  // DMMA m16n8k4: 512 FMA per warp-instruction, 4 independent accumulators
+  time_it([&] { dmma_k4_kernel<<<grid, blk>>>(d, iters); }, secs, b2, s2);
+  const double fl_k4 = 2.0 * 512 * 4 * iters * (double)grid.x * (blk.x / 32);
+  time_it([&] { dmma_k16_kernel<<<grid, blk>>>(d, iters); }, secs, b3, s3);
+  const double fl_k16 = 2.0 * 2048 * 2 * iters * (double)grid.x * (blk.x / 32);
   cudaError_t err = cudaGetLastError();
-  printf("{\"dfma_tflops\": %.3f, \"dmma_m16n8k4_tflops\": %.3f, \"dmma_m16n8k16_tflops\": %.3f, \"sms\": %d, \"err\": \"%s\"}\n",
-         dfma, dmma4, dmma16, sms, cudaGetErrorString(err));
+  printf("{\"dfma_tflops\": %.3f, \"dmma_m16n8k4_tflops\": %.3f, \"dmma_m16n8k16_tflops\": %.3f, "
+         "\"dfma_tflops_sustained\": %.3f, \"dmma_m16n8k4_tflops_sustained\": %.3f, "
+         "\"dmma_m16n8k16_tflops_sustained\": %.3f, \"sustained_seconds_per_kernel\": %.1f, \"sms\": %d, \"err\": \"%s\"}\n",
+         fl_dfma / (b1 * 1e-3) / 1e12, fl_k4 / (b2 * 1e-3) / 1e12, fl_k16 / (b3 * 1e-3) / 1e12,
+         fl_dfma / (s1 * 1e-3) / 1e12, fl_k4 / (s2 * 1e-3) / 1e12, fl_k16 / (s3 * 1e-3) / 1e12, secs, sms,
+         cudaGetErrorString(err));
   return 0;
 }
