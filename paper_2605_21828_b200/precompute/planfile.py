@@ -176,6 +176,43 @@ class PlanWriter:
                                      r_out_max=int(rec["r_out"].max())))
         self.stage = None
 
+    def add_stage_spooled(self, s, spool_path, ncoef, recs, idx_list):
+        """Write stage s whose coefficients were spooled to ``spool_path`` in
+        any block order (``recs`` = per block (kind, r_out, r_in, 0, idx_off,
+        spool_off) in canonical order, ``idx_list`` the index arrays in idx_off
+        order).  The coefficients are copied into canonical block order, so the
+        stage is laid out exactly as the stage-order writer lays it out.  Used
+        by the post-order builder (streaming.py)."""
+        assert self.stage is None
+        nl = 1 << self.L
+        assert len(recs) == nl
+        nidx = int(sum(a.size for a in idx_list))
+        self._write(struct.pack("<qqqq", s, nl, nidx, int(ncoef)))
+        out = []
+        cur = 0
+        isz = self.sdt.itemsize
+        with open(spool_path, "rb") as f:
+            for (kind, r_out, r_in, pad, idx_off, spool_off) in recs:
+                cnt = r_out * (r_in - r_out) if kind == KIND_ID else (r_out * r_in if kind == KIND_DENSE else 0)
+                if cnt:
+                    f.seek(int(spool_off) * isz)
+                    b = f.read(cnt * isz)
+                    if len(b) != cnt * isz:
+                        raise IOError("short spool")
+                    self._write(b)
+                out.append((kind, r_out, r_in, pad, idx_off, cur if cnt else 0))
+                cur += cnt
+        assert cur == int(ncoef)
+        rec = np.array(out, dtype=BLOCK_REC)
+        self._write(rec.tobytes())
+        idx = np.concatenate(idx_list) if idx_list else np.zeros(0, "<i4")
+        self._write(_pad8(idx.astype("<i4").tobytes()))
+        self.entries += int(ncoef)
+        kinds = rec["kind"]
+        self.stage_stats.append(dict(stage=s, ncoef=int(ncoef), n_identity=int((kinds == 0).sum()),
+                                     n_id=int((kinds == 1).sum()), n_dense=int((kinds == 2).sum()),
+                                     r_out_mean=float(rec["r_out"].mean()), r_out_max=int(rec["r_out"].max())))
+
     def close(self):
         assert self.stage is None
         self.f.seek(0)

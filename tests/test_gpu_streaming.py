@@ -1,0 +1,91 @@
+"""GPU parity of plans built by the streaming post-order factorization
+(§4, Alg. 3; precompute/streaming.py) at configs[0] (c1)
+and configs[3] (c4), and the builders' peak host memory.
+
+* libmht on the streaming plan vs the oracle's O2 on the same plan: element
+  by element, <= 1e-12 of each column's scale;
+* vs the dense sum O1 (all rows / modes): <= 10 x tol per column;
+* peak RSS of the streaming build (Phi arrives band by band from a file) vs
+  the stage-order builder holding Phi, each measured in a fresh process
+  (written to gpurun_out/streaming_rss.json when that directory exists).
+"""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import mht_inputs as mi
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _err(a, b):
+    out = 0.0
+    for r in range(b.shape[0]):
+        out = max(out, np.linalg.norm(a[r] - b[r]) / np.linalg.norm(b[r]),
+                  np.max(np.abs(a[r] - b[r])) / np.max(np.abs(b[r])))
+    return out
+
+
+def _rel(a, b):
+    return max(np.linalg.norm(a[r] - b[r]) / np.linalg.norm(b[r]) for r in range(b.shape[0]))
+
+
+def _build(name, out, mode):
+    r = subprocess.run([sys.executable, "-m", "paper_2605_21828_b200.precompute.streaming", name, out, mode],
+                       cwd=ROOT, capture_output=True, text=True, timeout=3000)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    return json.loads(lines[-1]) if lines else None
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a GPU")
+    from paper_2605_21828_b200 import _build as B, mht
+
+    B.build()
+    return mht
+
+
+def test_streaming_plans_c1_c4(gpu, oracle_lib, tmp_path):
+    rss = {}
+    for name in ("c1", "c4"):
+        w = mi.WORKLOADS[name]
+        sp = str(tmp_path / f"{name}_stream.plan")
+        if w.family == "mesh":
+            _build(name, sp, "prepare")  # eigenvectors -> band file (GPU eigensolver), separate process
+        rss[name] = {"streaming": _build(name, sp, "streaming"),
+                     "stage_order_resident_phi": _build(name, str(tmp_path / f"{name}_stage.plan"), "stage")}
+        P = gpu.Plan(sp)
+        O = oracle_lib.Plan(sp)
+        for nrhs in sorted(set((1,) + tuple(w.nrhs))):
+            c = mi.workload_coefficients(w, nrhs)
+            y = mi.workload_adjoint_input(w, nrhs)
+            f = P.apply(torch.from_numpy(c).cuda()).cpu().numpy()
+            a = P.adjoint(torch.from_numpy(y).cuda()).cpu().numpy()
+            assert _err(f, O.apply(c)) <= 1e-12, (name, nrhs)
+            assert _err(a, O.adjoint(y)) <= 1e-12, (name, nrhs)
+            sub = slice(0, min(nrhs, 2))
+            if w.family == "flat":
+                x = mi.flat_points(w.n)
+                k = mi.flat_modes(w.extra["side"])[: w.m]
+                fd, cd = oracle_lib.flat_synth(x, k, c[sub]), oracle_lib.flat_analysis(x, k, y[sub])
+            else:
+                from paper_2605_21828_b200.precompute.streaming import BandFile
+
+                Phi = BandFile(sp + ".bands", w.n, w.m, np.float64)(0, w.m).copy()
+                fd, cd = oracle_lib.dense_synth(Phi, c[sub]), oracle_lib.dense_analysis(Phi, y[sub])
+            assert _rel(f[sub], fd) <= 10 * w.tol, (name, nrhs, _rel(f[sub], fd))
+            assert _rel(a[sub], cd) <= 10 * w.tol, (name, nrhs, _rel(a[sub], cd))
+        P.close()
+        assert rss[name]["streaming"]["peak_rss_MB"] < rss[name]["stage_order_resident_phi"]["peak_rss_MB"]
+    if os.path.isdir(os.path.join(ROOT, "gpurun_out")):
+        json.dump(rss, open(os.path.join(ROOT, "gpurun_out", "streaming_rss.json"), "w"), indent=1)
