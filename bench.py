@@ -255,7 +255,7 @@ def run_cpu_table(args, w, path):
     rows = np.arange(w.n) if w.n * w.m <= 2**27 else np.sort(np.random.default_rng(7).choice(w.n, 4096, replace=False))
     t0 = time.perf_counter()
     if w.family == "flat":
-        oracle.flat_synth(mi.flat_points(w.n)[rows], mi.flat_modes(w.extra["side"])[: w.m], c)
+        oracle.flat_synth(mi.flat_points(w.n)[rows], mi.flat_workload_modes(w), c)
     elif w.family == "sphere":
         th, ph, _ = mi.sphere_points(w.n)
         oracle.sphere_synth(th[rows], ph[rows], w.extra["lmax"], c)

@@ -65,6 +65,34 @@ def flat_modes(side: int) -> np.ndarray:
     return np.stack([k1[order], k2[order]], axis=1)
 
 
+def flat_modes_kd(side: int, L: int) -> np.ndarray:
+    """The modes of [-side/2, side/2 - 1]^2 (side a power of two) in the order of
+    a 2-D kd tree over the FREQUENCY box (the quadtree-in-frequency variant,
+    PAPER.md §5): depth d halves the current box along k1 (d even) or
+    k2 (d odd) at its midpoint, so the nodes at even depths are exactly the
+    quadtree's squares; 2^L leaves of side^2 / 2^L modes, each leaf in
+    eigenvalue order (|k|^2, k1, k2) inside.  Returns (side^2, 2) int64."""
+    s = int(round(math.log2(side)))
+    assert 1 << s == side and 0 <= L <= 2 * s
+    h = side // 2
+    k = flat_modes(side)
+    i1, i2 = k[:, 0] + h, k[:, 1] + h           # 0 .. side - 1
+    leaf = np.zeros(k.shape[0], dtype=np.int64)
+    for d in range(L):                          # bit d of the path: axis d % 2, split number d // 2
+        bit = ((i1 if d % 2 == 0 else i2) >> (s - 1 - d // 2)) & 1
+        leaf = (leaf << 1) | bit
+    order = np.argsort(leaf, kind="stable")     # stable: eigenvalue order inside a leaf
+    return k[order].copy()
+
+
+def flat_workload_modes(w) -> np.ndarray:
+    """The mode list (c order) of a flat workload: eigenvalue order (reading A7/A8)
+    or, for extra["ftree"] == "kd", the 2-D kd (quadtree) frequency order."""
+    if w.extra.get("ftree") == "kd":
+        return flat_modes_kd(w.extra["side"], w.L)[: w.m]
+    return flat_modes(w.extra["side"])[: w.m]
+
+
 def flat_modes_first(m: int) -> np.ndarray:
     """The first m modes of Z^2 in eigenvalue order (for m not a square)."""
     side = 2 * int(math.ceil(math.sqrt(m) / 2.0 + 2))
@@ -172,6 +200,13 @@ WORKLOADS = {
     "c4": Workload("c4", "mesh", 32768, 2048, "float64", 1e-8, 5, (1, 64), {"nu": 256, "nv": 128}),
     # configs[4]: flat, n = m = 2^20, k in [-512,511]^2, tol 1e-6, nrhs 1 and 16
     "c5": Workload("c5", "flat", 1 << 20, 1 << 20, "complex128", 1e-6, 14, (1, 16), {"side": 1024}),
+    # labelled stand-in for configs[4] (SURVEY.md §8(d) c5 protocol step 3): the largest flat
+    # square whose plan fits one B200 — n = m = 2^18, k in [-256,255]^2, tol 1e-6, nrhs 1 and 16
+    "c5s": Workload("c5s", "flat", 1 << 18, 1 << 18, "complex128", 1e-6, 12, (1, 16), {"side": 512}),
+    # the quadtree-in-frequency plan variant (§5; NEXT-3): configs[0] / [1]
+    # with the frequency tree a 2-D kd tree over the frequency box instead of eigenvalue ranges
+    "c1kd": Workload("c1kd", "flat", 4096, 4096, "complex128", 1e-8, 6, (1,), {"side": 64, "ftree": "kd"}),
+    "c2kd": Workload("c2kd", "flat", 65536, 65536, "complex128", 1e-8, 10, (1, 32), {"side": 256, "ftree": "kd"}),
 }
 
 
@@ -187,7 +222,7 @@ def workload_points(w: Workload):
 
 def workload_modes(w: Workload):
     if w.family == "flat":
-        return flat_modes(w.extra["side"])
+        return flat_workload_modes(w)
     if w.family == "sphere":
         return sphere_modes(w.extra["lmax"])
     raise ValueError("mesh modes are eigen-indices 0..m-1")

@@ -93,8 +93,16 @@ def build_plan_streaming(bands, perm, sp_off, fr_off, L, tol, path, seed=1234, w
     sp_off = np.asarray(sp_off, dtype=np.int64)
     fr_off = np.asarray(fr_off, dtype=np.int64)
     sdt = np.dtype("<c16") if dtype == np.complex128 else np.dtype("<f8")
-    workers = workers or max(1, min(16, os.cpu_count() or 1))
+    workers = workers or max(1, min(8, os.cpu_count() or 1))
     pool = ThreadPoolExecutor(workers) if workers > 1 else None
+    # parallelism comes from the block pool: single-threaded BLAS inside it
+    # (nested BLAS threads would also multiply the per-thread work buffers)
+    try:
+        from threadpoolctl import threadpool_limits
+
+        _tpl = threadpool_limits(1)
+    except Exception:
+        _tpl = None
     spool_dir = spool_dir or os.path.dirname(os.path.abspath(path))
     spools = [tempfile.NamedTemporaryFile("wb", dir=spool_dir, prefix=".bfspool", delete=False) for _ in range(L + 2)]
     ncoef = [0] * (L + 2)
@@ -185,6 +193,8 @@ def build_plan_streaming(bands, perm, sp_off, fr_off, L, tol, path, seed=1234, w
     finally:
         if pool is not None:
             pool.shutdown()
+        if _tpl is not None:
+            _tpl.unregister()
         for f in spools:
             f.close()
     # ---- assemble the plan in stage order from the spools
@@ -230,7 +240,7 @@ def _main():
     name, out = sys.argv[1], sys.argv[2]
     mode = sys.argv[3] if len(sys.argv) > 3 else "streaming"  # streaming | stage | prepare (mesh band file)
     w = mi.WORKLOADS[name] if name in mi.WORKLOADS else None
-    band_path = out + ".bands"
+    band_path = sys.argv[4] if len(sys.argv) > 4 else out + ".bands"  # mesh: the shared band file
     t0 = time.time()
     if w.family == "mesh":
         # the eigenvectors come from the eigensolver once, to a band file on disk

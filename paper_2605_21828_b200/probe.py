@@ -1,25 +1,31 @@
-"""Plan-size probe for workloads too large to factorize (configs[4]: flat,
-n = m = 2^20, tol 1e-6).  SURVEY.md §8(d) "Config 5 protocol".
+"""Plan-size probe for flat workloads too large to factorize here (configs[4]:
+n = m = 2^20, tol 1e-6) and for sizing the largest stand-in that fits one
+B200.  SURVEY.md §8(d) "Config 5 protocol", step 1.
 
-For each level l, sample blocks Phi(tau, nu) (tau a space node at depth l of
-the median kd tree, nu a frequency node at height l spread over the annulus
-radii), compute their eps-rank exactly from the eigenvalues of the Gram
-matrix on the GPU (#{sigma_i > eps sigma_1}, the relative ID criterion), and
-extrapolate the level's stored coefficients as
+Per level l = 0..L the probe samples S transfer blocks (frequency nodes nu at
+height l stratified over the whole eigenvalue range — the annulus radii — and
+a random space node tau at depth l) and measures, with the GPU builder's own
+rank criterion (gpu_builder.cpqr_batched: column-pivoted Householder QR, rank
+= first j with |R_jj| <= tol |R_00|, reading A5; tall blocks on a Gaussian row
+sketch of cols + 16 rows, exactly as the builder does):
 
-    2^L * mean(r_out * (r_in - r_out)),   r_in = 2 * mean r_out(l - 1)
+    r_out = rank Phi(tau, nu),
+    r_in  = rank Phi(p, c1) + rank Phi(p, c2)   (p = parent of tau, c1, c2 = children of nu),
 
-(IDENTITY when r_out = r_in), plus the leaf factors U (n * r_L).  The paper
-states the rank bounds of §5 only asymptotically; this
-probe measures the actual ranks of this workload.
+so each sample gives the block's stored coefficients r_out (r_in - r_out)
+(0 when r_out = r_in: IDENTITY).  The level's estimate is 2^L x the sample
+mean; the leaf factors add sum_tau |tau| r_L(tau) ~ n x mean rank Phi(tau, all).
+A row / column subset would only lower a rank, so no block is subsampled.
+The paper states the rank bounds of §5 only asymptotically; the
+probe measures this workload's ranks.  Validated on configs[1], whose plan is
+built (profiles/r02_probe_c2.json vs the plan's stage sizes).
 
-    python -m paper_2605_21828_b200.probe --workload c5 --samples 6 > probe.json
+    python -m paper_2605_21828_b200.probe --workload c5 --samples 16 > probe.json
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import sys
 import time
 
@@ -27,81 +33,104 @@ import numpy as np
 
 import mht_inputs as mi
 
+from .precompute.gpu_builder import OVERSAMPLE, TorchFlatBasis, cpqr_batched
 from .precompute.trees import freq_tree, kd_tree
 
 
-def eps_rank_gram(A, eps):
+def block_rank(basis, rows, cols, tol, gen):
+    """The builder's rank of Phi(rows, cols) (gpu_builder._cpqr_group)."""
     import torch
 
-    r, c = A.shape
-    G = A.conj().T @ A if c <= r else A @ A.conj().T
-    ev = torch.linalg.eigvalsh(G).clamp(min=0).sqrt()
-    s1 = ev[-1]
-    return int((ev > eps * s1).sum().item())
+    dev = basis.x.device
+    r = torch.as_tensor(np.asarray(rows, np.int64), device=dev)[None, :]
+    c = torch.as_tensor(np.asarray(cols, np.int64), device=dev)[None, :]
+    At = basis.block_t(r, c)                                   # (1, C, R)
+    C, R = At.shape[1], At.shape[2]
+    if R >= 4 * C and R > C + OVERSAMPLE:
+        ks = C + OVERSAMPLE
+        G = torch.complex(torch.randn((1, R, ks), generator=gen, device=dev, dtype=torch.float64),
+                          torch.randn((1, R, ks), generator=gen, device=dev, dtype=torch.float64))
+        At = torch.bmm(At, G)
+        del G
+    ranks, _ = cpqr_batched(At, tol)
+    out = int(min(int(ranks[0]), C))
+    del At
+    return out
 
 
-def probe(w: mi.Workload, samples: int = 6, seed: int = 0, device="cuda", log=print):
+def probe(w: mi.Workload, samples: int = 16, seed: int = 0, device="cuda", log=print):
     import torch
 
     n, m, L, tol = w.n, w.m, w.L, w.tol
-    x = mi.flat_points(n)
-    k = mi.flat_modes(w.extra["side"])
+    x = mi.flat_points(n, seed=w.extra.get("seed", mi.SEED_GEOMETRY))
+    k = mi.flat_workload_modes(w)
     t0 = time.time()
-    perm, sp_off = kd_tree(x, L)
+    perm, sp_off = kd_tree(x, L, alternate=True)
     fr_off = freq_tree(m, L)
     log(f"[probe] trees in {time.time() - t0:.1f}s")
-    X = torch.as_tensor(x, device=device)
-    Kt = torch.as_tensor(k.astype(np.float64), device=device)
+    basis = TorchFlatBasis(x, k, device)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(1234 + seed)
     rng = np.random.default_rng(seed)
     nl = 1 << L
+
+    def rows_of(d, t):
+        wd = 1 << (L - d)
+        return perm[sp_off[t * wd]: sp_off[(t + 1) * wd]]
+
+    def cols_of(h, v):
+        wh = 1 << h
+        return np.arange(fr_off[v * wh], fr_off[(v + 1) * wh])
+
     levels = []
-    r_prev = 64.0
-    total = 0
+    total = 0.0
     for l in range(0, L + 1):
         nf = nl >> l
-        w_sp = 1 << (L - l)
-        vs = np.unique(np.linspace(0, nf - 1, min(samples, nf)).round().astype(int))
-        ranks, shapes = [], []
         t1 = time.time()
+        vs = np.unique(((np.arange(samples) + rng.uniform(size=samples)) * nf / samples).astype(int).clip(0, nf - 1))
+        ent, r_outs, r_ins = [], [], []
         for v in vs:
             t = int(rng.integers(0, 1 << l))
-            rows = perm[sp_off[t * w_sp]: sp_off[(t + 1) * w_sp]]
-            cols = np.arange(fr_off[v * (1 << l)], fr_off[(v + 1) * (1 << l)])
-            # cap the sampled block at 16k x 16k (a row subsample only lowers the rank estimate
-            # when rows > 16k, where blocks are tall and full column rank anyway)
-            if rows.size > 16384:
-                rows = np.sort(rng.choice(rows, 16384, replace=False))
-            ph = X[torch.as_tensor(rows, device=device)] @ Kt[torch.as_tensor(cols, device=device)].T
-            A = torch.polar(torch.ones_like(ph), ph)
-            ranks.append(eps_rank_gram(A, tol))
-            shapes.append((int(rows.size), int(cols.size)))
-            del A, ph
-        r_out = float(np.mean(ranks))
-        r_in = 64.0 if l == 0 else 2.0 * r_prev
-        r_out = min(r_out, r_in)
-        ident = r_out >= r_in - 0.5
-        entries = 0.0 if ident else nl * r_out * (r_in - r_out)
-        total += entries
-        levels.append({"level": l, "blocks": nl, "block_rows": int(n >> l), "block_cols": int(64 << l),
-                       "sampled_ranks": ranks, "r_out_mean": r_out, "r_in_est": r_in,
-                       "identity": bool(ident), "entries_est": entries, "seconds": round(time.time() - t1, 1)})
-        log(f"[probe] level {l}: ranks {ranks} -> r_out {r_out:.0f}, r_in {r_in:.0f}, entries {entries:.3g}")
-        r_prev = r_out
-    u_entries = n * r_prev
+            r_out = block_rank(basis, rows_of(l, t), cols_of(l, v), tol, gen)
+            if l == 0:
+                r_in = len(cols_of(0, v))
+            else:
+                p = t >> 1
+                r_in = (block_rank(basis, rows_of(l - 1, p), cols_of(l - 1, 2 * v), tol, gen)
+                        + block_rank(basis, rows_of(l - 1, p), cols_of(l - 1, 2 * v + 1), tol, gen))
+            r_out = min(r_out, r_in)
+            r_outs.append(r_out)
+            r_ins.append(r_in)
+            ent.append(0 if r_out == r_in else r_out * (r_in - r_out))
+        lev = nl * float(np.mean(ent))
+        total += lev
+        levels.append({"level": l, "blocks": nl, "block_rows": int(n >> l), "block_cols": int(m >> (L - l)),
+                       "samples": len(vs), "r_out": r_outs, "r_in": r_ins,
+                       "r_out_mean": float(np.mean(r_outs)), "identity_fraction": float(np.mean(np.array(ent) == 0)),
+                       "entries_est": lev, "entries_sem": nl * float(np.std(ent) / np.sqrt(len(ent))),
+                       "seconds": round(time.time() - t1, 1)})
+        log(f"[probe] level {l}: r_out mean {np.mean(r_outs):.0f} (min {min(r_outs)}, max {max(r_outs)}), "
+            f"entries {lev:.3g} ({time.time() - t1:.1f}s)")
+        torch.cuda.empty_cache()
+    # leaf factors U_tau = Phi(tau, J_tau), r_L(tau) = rank Phi(tau, all) <= |tau|
+    uts = rng.integers(0, nl, size=min(samples, nl))
+    u = [len(rows_of(L, int(t))) * block_rank(basis, rows_of(L, int(t)), np.arange(m), tol, gen) for t in uts]
+    u_entries = nl * float(np.mean(u))
     total += u_entries
     sb = 16
-    out = {"workload": w.name, "n": n, "m": m, "L": L, "tol": tol, "samples_per_level": samples,
-           "levels": levels, "U_entries_est": u_entries, "entries_est": total,
-           "plan_bytes_est": total * sb, "dense_bytes": n * m * sb,
-           "fits_one_b200": total * sb < 150e9,
-           "hbm_bytes": 183359 * 2**20}
-    return out
+    sem = float(np.sqrt(sum(lv["entries_sem"] ** 2 for lv in levels)))
+    return {"workload": w.name, "n": n, "m": m, "L": L, "tol": tol, "samples_per_level": samples,
+            "rank_method": "builder CPQR (gpu_builder.cpqr_batched; tall blocks on a cols+16 Gaussian row sketch)",
+            "levels": levels, "U_entries_est": u_entries, "entries_est": total, "entries_sem": sem,
+            "plan_bytes_est": total * sb, "plan_bytes_sem": sem * sb, "dense_bytes": n * m * sb,
+            "fits_one_b200": total * sb < 150e9, "hbm_bytes": 183359 * 2**20,
+            "seconds": round(time.time() - t0, 1)}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c5")
-    ap.add_argument("--samples", type=int, default=6)
+    ap.add_argument("--samples", type=int, default=16)
     a = ap.parse_args()
     res = probe(mi.WORKLOADS[a.workload], a.samples, log=lambda s: print(s, file=sys.stderr, flush=True))
     print(json.dumps(res))

@@ -30,7 +30,7 @@ def setup(w: mi.Workload):
     """Return (basis, perm, sp_off, fr_off)."""
     if w.family == "flat":
         x = mi.flat_points(w.n, seed=w.extra.get("seed", mi.SEED_GEOMETRY))
-        k = mi.flat_modes(w.extra["side"])[: w.m]
+        k = mi.flat_workload_modes(w)
         basis = FlatBasis(x, k)
         perm, sp_off = kd_tree(x, w.L, alternate=True)
     elif w.family == "sphere":

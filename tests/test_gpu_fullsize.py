@@ -67,7 +67,17 @@ def test_config2_flat_65536_full_size(gpu, oracle_lib):
     """configs[1]: flat, n = m = 65,536, tol 1e-8, nrhs 1 and 32."""
     w = mi.WORKLOADS["c2"]
     x = mi.flat_points(w.n)
-    k = mi.flat_modes(w.extra["side"])
+    k = mi.flat_workload_modes(w)
+    _run(gpu, oracle_lib, w,
+         lambda rows, c: oracle_lib.flat_synth(x[rows], k, c),
+         lambda cols, y: oracle_lib.flat_analysis(x, k[cols], y))
+
+
+def test_config2_quadtree_frequency_variant_full_size(gpu, oracle_lib):
+    """NEXT-3: configs[1] with the 2-D kd (quadtree) frequency tree, nrhs 1 and 32."""
+    w = mi.WORKLOADS["c2kd"]
+    x = mi.flat_points(w.n)
+    k = mi.flat_workload_modes(w)
     _run(gpu, oracle_lib, w,
          lambda rows, c: oracle_lib.flat_synth(x[rows], k, c),
          lambda cols, y: oracle_lib.flat_analysis(x, k[cols], y))

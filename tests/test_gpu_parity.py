@@ -98,7 +98,7 @@ def check_plan(gpu, oracle_lib, path, w, nrhs_list=(1,), dense=None):
 
 def flat_dense(oracle_lib, w):
     x = mi.flat_points(w.n)
-    k = mi.flat_modes(w.extra["side"])[: w.m]
+    k = mi.flat_workload_modes(w)
     return lambda c, y: (oracle_lib.flat_synth(x, k, c), oracle_lib.flat_analysis(x, k, y))
 
 
@@ -119,6 +119,16 @@ def test_config1_full_parity(gpu, oracle_lib, plans):
     path = str(plans / "c1.plan")
     W.build_workload_plan(w, path, workers=8, log=None)
     check_plan(gpu, oracle_lib, path, w, (1, 4), dense=flat_dense(oracle_lib, w))
+
+
+def test_config1_quadtree_frequency_variant(gpu, oracle_lib, plans):
+    """NEXT-3 (§5): configs[0] with the frequency tree a 2-D
+    kd tree over the frequency box (quadtree squares at even depths): full
+    parity vs O2 element by element and vs the dense sum within 10 x tol."""
+    w = mi.WORKLOADS["c1kd"]
+    path = str(plans / "c1kd.plan")
+    W.build_workload_plan(w, path, workers=8, log=None)
+    check_plan(gpu, oracle_lib, path, w, (1, 4, 32), dense=flat_dense(oracle_lib, w))
 
 
 def test_sphere_parity(gpu, oracle_lib, plans):

@@ -37,8 +37,8 @@ def _rel(a, b):
     return max(np.linalg.norm(a[r] - b[r]) / np.linalg.norm(b[r]) for r in range(b.shape[0]))
 
 
-def _build(name, out, mode):
-    r = subprocess.run([sys.executable, "-m", "paper_2605_21828_b200.precompute.streaming", name, out, mode],
+def _build(name, out, mode, bands):
+    r = subprocess.run([sys.executable, "-m", "paper_2605_21828_b200.precompute.streaming", name, out, mode, bands],
                        cwd=ROOT, capture_output=True, text=True, timeout=3000)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
@@ -60,10 +60,11 @@ def test_streaming_plans_c1_c4(gpu, oracle_lib, tmp_path):
     for name in ("c1", "c4"):
         w = mi.WORKLOADS[name]
         sp = str(tmp_path / f"{name}_stream.plan")
+        bands = str(tmp_path / f"{name}.bands")
         if w.family == "mesh":
-            _build(name, sp, "prepare")  # eigenvectors -> band file (GPU eigensolver), separate process
-        rss[name] = {"streaming": _build(name, sp, "streaming"),
-                     "stage_order_resident_phi": _build(name, str(tmp_path / f"{name}_stage.plan"), "stage")}
+            _build(name, sp, "prepare", bands)  # eigenvectors -> band file (GPU eigensolver), separate process
+        rss[name] = {"streaming": _build(name, sp, "streaming", bands),
+                     "stage_order_resident_phi": _build(name, str(tmp_path / f"{name}_stage.plan"), "stage", bands)}
         P = gpu.Plan(sp)
         O = oracle_lib.Plan(sp)
         for nrhs in sorted(set((1,) + tuple(w.nrhs))):
@@ -76,12 +77,12 @@ def test_streaming_plans_c1_c4(gpu, oracle_lib, tmp_path):
             sub = slice(0, min(nrhs, 2))
             if w.family == "flat":
                 x = mi.flat_points(w.n)
-                k = mi.flat_modes(w.extra["side"])[: w.m]
+                k = mi.flat_workload_modes(w)
                 fd, cd = oracle_lib.flat_synth(x, k, c[sub]), oracle_lib.flat_analysis(x, k, y[sub])
             else:
                 from paper_2605_21828_b200.precompute.streaming import BandFile
 
-                Phi = BandFile(sp + ".bands", w.n, w.m, np.float64)(0, w.m).copy()
+                Phi = BandFile(bands, w.n, w.m, np.float64)(0, w.m).copy()
                 fd, cd = oracle_lib.dense_synth(Phi, c[sub]), oracle_lib.dense_analysis(Phi, y[sub])
             assert _rel(f[sub], fd) <= 10 * w.tol, (name, nrhs, _rel(f[sub], fd))
             assert _rel(a[sub], cd) <= 10 * w.tol, (name, nrhs, _rel(a[sub], cd))
