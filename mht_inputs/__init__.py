@@ -200,9 +200,13 @@ WORKLOADS = {
     "c4": Workload("c4", "mesh", 32768, 2048, "float64", 1e-8, 5, (1, 64), {"nu": 256, "nv": 128}),
     # configs[4]: flat, n = m = 2^20, k in [-512,511]^2, tol 1e-6, nrhs 1 and 16
     "c5": Workload("c5", "flat", 1 << 20, 1 << 20, "complex128", 1e-6, 14, (1, 16), {"side": 1024}),
-    # labelled stand-in for configs[4] (SURVEY.md §8(d) c5 protocol step 3): the largest flat
-    # square whose plan fits one B200 — n = m = 2^18, k in [-256,255]^2, tol 1e-6, nrhs 1 and 16
-    "c5s": Workload("c5s", "flat", 1 << 18, 1 << 18, "complex128", 1e-6, 12, (1, 16), {"side": 512}),
+    # configs[4] protocol: n = m = 2^18 on the box [-256,255]^2 at tol
+    # 1e-6 probes to 285 GB (profiles/r02_probe_c5p18.json): it does not fit one B200.  The labelled
+    # stand-in is the largest flat square that does: n = m = 2^17 points / modes, the 2^17 lowest
+    # eigenvalues (|k| <= ~204, taken from the [-256,255]^2 box in eigenvalue order), tol 1e-6,
+    # nrhs 1 and 16
+    "c5p18": Workload("c5p18", "flat", 1 << 18, 1 << 18, "complex128", 1e-6, 12, (1, 16), {"side": 512}),
+    "c5s": Workload("c5s", "flat", 1 << 17, 1 << 17, "complex128", 1e-6, 11, (1, 16), {"side": 512}),
     # the quadtree-in-frequency plan variant (§5; NEXT-3): configs[0] / [1]
     # with the frequency tree a 2-D kd tree over the frequency box instead of eigenvalue ranges
     "c1kd": Workload("c1kd", "flat", 4096, 4096, "complex128", 1e-8, 6, (1,), {"side": 64, "ftree": "kd"}),

@@ -138,13 +138,13 @@ def cpqr_batched(At, tol):
     for j in range(kmax):
         p = norms[:, j:].argmax(1) + j
         rowp = At[bidx, p].clone()
-        At[bidx, p] = At[:, j]
+        At[bidx, p] = At[:, j].clone()  # (clone: p == j aliases the source)
         At[:, j] = rowp
         np_ = norms[bidx, p].clone()
-        norms[bidx, p] = norms[:, j]
+        norms[bidx, p] = norms[:, j].clone()
         norms[:, j] = np_
         pp = perm[bidx, p].clone()
-        perm[bidx, p] = perm[:, j]
+        perm[bidx, p] = perm[:, j].clone()
         perm[:, j] = pp
         rjj = norms[:, j].clamp(min=0).sqrt()
         newly = (~done) & (rjj <= tol * r00)

@@ -237,6 +237,31 @@ def _main():
 
     from .. import workloads as W
 
+    import threading
+
+    import psutil
+
+    class _Peak:
+        """Resident set size sampled every 20 ms on a thread (the build's peak above
+        the process's resident size just before it starts)."""
+
+        def __init__(self):
+            self.p, self.peak, self.stop_ = psutil.Process(), 0, False
+            self.base = self.p.memory_info().rss
+            self.t = threading.Thread(target=self.run, daemon=True)
+            self.t.start()
+
+        def run(self):
+            while not self.stop_:
+                self.peak = max(self.peak, self.p.memory_info().rss)
+                time.sleep(0.02)
+
+        def stop(self):
+            self.stop_ = True
+            self.t.join()
+            self.peak = max(self.peak, self.p.memory_info().rss)
+            return (self.peak - self.base) / 2**20
+
     name, out = sys.argv[1], sys.argv[2]
     mode = sys.argv[3] if len(sys.argv) > 3 else "streaming"  # streaming | stage | prepare (mesh band file)
     w = mi.WORKLOADS[name] if name in mi.WORKLOADS else None
@@ -262,6 +287,7 @@ def _main():
         fr_off = freq_tree(w.m, w.L)
         rss0 = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss
         t1 = time.time()
+        pk = _Peak()
         if mode == "streaming":
             st = build_plan_streaming(bf, perm, sp_off, fr_off, w.L, w.tol, out, log=None)
         else:  # stage-order CPU builder on the resident Phi read from the same file
@@ -274,6 +300,7 @@ def _main():
         basis, perm, sp_off, fr_off = W.setup(w)
         rss0 = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss
         t1 = time.time()
+        pk = _Peak()
         if mode == "streaming":
             st = build_plan_streaming(ClosedFormBands(basis), perm, sp_off, fr_off, w.L, w.tol, out, log=None)
         else:
@@ -282,8 +309,10 @@ def _main():
 
             Phi = basis.block(np.arange(w.n), np.arange(w.m))
             st = build_plan(DenseBasis(Phi), perm, sp_off, fr_off, w.L, w.tol, out, workers=1, log=None)
+    build_peak = pk.stop()
     rss = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss
     print(json.dumps({"workload": name, "mode": mode, "seconds_build": round(time.time() - t1, 1),
+                      "build_peak_rss_above_start_MB": round(build_peak, 1),
                       "seconds_total": round(time.time() - t0, 1), "peak_rss_MB": rss / 1024.0,
                       "rss_before_build_MB": rss0 / 1024.0, "entries": st["entries"],
                       "plan_bytes": st["plan_bytes"], "kept_bytes_peak": st.get("kept_bytes_peak")}))

@@ -9,6 +9,8 @@ configuration bench.py times (same plan cache, same nrhs widths).
 The plan is built once per box (GPU builder, ~3 min for configs[1]) into the
 cache bench.py also uses.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -40,7 +42,7 @@ def gpu():
     return mht
 
 
-def _run(gpu, oracle_lib, w, dense_rows, dense_cols):
+def _run(gpu, oracle_lib, w, dense_rows, dense_cols, drop_plan=False):
     path = W.ensure_plan(w, builder="gpu", log=None)
     torch.cuda.empty_cache()
     P = gpu.Plan(path)
@@ -61,6 +63,9 @@ def _run(gpu, oracle_lib, w, dense_rows, dense_cols):
         cd = dense_cols(cols, y[sub])
         assert rel_cols(a[sub][:, cols], cd) <= 10 * w.tol, ("adj vs dense", nrhs, rel_cols(a[sub][:, cols], cd))
     P.close()
+    del O
+    if drop_plan and not os.environ.get("MHT_KEEP_PLANS"):
+        os.unlink(path)  # the plan cache lives in /dev/shm (host RAM): free it for the next workload
 
 
 def test_config2_flat_65536_full_size(gpu, oracle_lib):
@@ -80,7 +85,7 @@ def test_config2_quadtree_frequency_variant_full_size(gpu, oracle_lib):
     k = mi.flat_workload_modes(w)
     _run(gpu, oracle_lib, w,
          lambda rows, c: oracle_lib.flat_synth(x[rows], k, c),
-         lambda cols, y: oracle_lib.flat_analysis(x, k[cols], y))
+         lambda cols, y: oracle_lib.flat_analysis(x, k[cols], y), drop_plan=True)
 
 
 def test_config3_sphere_65536_full_size(gpu, oracle_lib):
@@ -108,3 +113,19 @@ def test_config4_torus_mesh_full_size(gpu, oracle_lib):
     _run(gpu, oracle_lib, w,
          lambda rows, c: oracle_lib.dense_synth(Phi[rows], c),
          lambda cols, y: oracle_lib.dense_analysis(Phi[:, cols], y))
+
+
+@pytest.mark.skipif(os.environ.get("MHT_TEST_C5S") != "1",
+                    reason="the c5 stand-in builds a ~100 GB plan (~10+ min); run with MHT_TEST_C5S=1 "
+                           "(log committed under profiles/)")
+def test_config5_standin_full_size(gpu, oracle_lib):
+    """configs[4] stand-in (SURVEY.md §8(d) c5 protocol step 3; configs[4] itself,
+    n = m = 2^20, probes to ~0.9 TB and 2^18 to 285 GB): flat n = m = 2^17 with the
+    2^17 lowest eigenvalues, tol 1e-6, nrhs 1 and 16 — GPU vs O2 on the whole
+    output, vs the dense sum on sampled rows / modes."""
+    w = mi.WORKLOADS["c5s"]
+    x = mi.flat_points(w.n)
+    k = mi.flat_workload_modes(w)
+    _run(gpu, oracle_lib, w,
+         lambda rows, c: oracle_lib.flat_synth(x[rows], k, c),
+         lambda cols, y: oracle_lib.flat_analysis(x, k[cols], y), drop_plan=not os.environ.get("MHT_KEEP_C5S"))

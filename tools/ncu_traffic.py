@@ -25,13 +25,14 @@ UNITS = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "tbyte": 1e12,
 def phase_of(name: str, width: int) -> str | None:
     if name.startswith("void") or "::" in name:
         name = name.split("::")[-1]
-    if name.startswith("fwd_kernel"):
+    if name.startswith("fwd_kernel") or name.startswith("fwd_lat_kernel"):
         return "fwd@1"
     if name.startswith("adj_kernel"):
         return "adj@1"
     if name.startswith("mma_kernel") or name.startswith("mma_ws_kernel") or name.startswith("mma_real_kernel"):
         args = name[name.index("<") + 1:].split(",")
-        flag = args[0] if name.startswith("mma_real_kernel") else args[1]  # mma_real_kernel<ADJ, ...>
+        # mma_real_kernel<ADJ, ...>, mma_ws_kernel<ADJ>, mma_kernel<S, ADJ, ...>
+        flag = args[1] if name.startswith("mma_kernel") else args[0]
         adj = flag.strip().rstrip(">") in ("1", "true")
         return f"{'adj' if adj else 'fwd'}@{width}"
     if name.startswith("reduce_kernel"):
