@@ -418,9 +418,7 @@ def main():
                 "frac": achieved / peaks["dmma_tflops"], "frac_of_burst_peak": achieved / peaks["dmma_tflops_burst"],
                 "frac_of_nominal": achieved / (148 * 64 * 2 * 1.965e9 / 1e12),  # 37.2 TF: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz
                 "traffic": traffic, "algorithmic_flops_per_launch": alg,
-                "kernel": (f"{'mma_ws_kernel' if P.is_complex else 'mma_real_kernel'} {dkind} nrhs={dr} "
-                           f"(DMMA m16n8k4 f64, "
-                           f"{'TMA + warp-specialised' if P.is_complex else 'cp.async ring, 6 CTAs/SM'})"),
+                "kernel": _mma_kernel_name(P.is_complex, dkind, dr),
                 "peak_source": peaks["dmma_src"]}
         if P.is_complex:
             roof["note"] = ("achieved counts 8 real flops per complex multiply-add (algorithmic); the kernel "
@@ -603,6 +601,16 @@ def _e2e(P, phases, w, ws, args, device_ms_per_step=None):
         out["copy_floor_ms_per_step"] = 1e3 * (h2d / (rates["h2d"] * 1e9) + d2h / (rates["d2h"] * 1e9))
         out["device_ms_per_step"] = device_ms_per_step
     return out
+
+
+def _mma_kernel_name(cplx, kind, nrhs):
+    """The multi-RHS kernel libmht dispatches for this width (csrc/mht_kernels.cu mma_dispatch)."""
+    if cplx and nrhs >= 16:
+        return (f"mma_ws_kernel {kind} nrhs={nrhs} (DMMA m16n8k4 f64, TMA + warp-specialised, "
+                f"{32 if nrhs >= 32 else 16} RHS per CTA)")
+    if not cplx and nrhs >= 32:
+        return f"mma_real_kernel {kind} nrhs={nrhs} (DMMA m16n8k4 f64, cp.async ring, 6 CTAs/SM)"
+    return f"mma_kernel {kind} nrhs={nrhs} (DMMA m16n8k4 f64, {16 if nrhs >= 16 else 8} RHS per CTA)"
 
 
 def _peaks():

@@ -145,8 +145,7 @@ void lsqr_xnorm(bool cplx, const void *x, int64_t len, int k, double *partial, L
 // latency: the few-tile variant (x staged per chunk, balanced batches, L2
 // prefetch) instead of the streaming one; the loader picks per stage.
 void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool latency, void *stream);
-void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
-                void *stream);
+void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f, void *stream);
 // multi-RHS (nrhs >= 2): DMMA kernels; forward uses the 64-row tiles, the
 // adjoint uses 64-column tiles (adjm lists).
 void launch_mma(bool is_complex, bool adjoint, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,

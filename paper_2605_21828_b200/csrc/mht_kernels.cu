@@ -652,7 +652,9 @@ __global__ void __launch_bounds__(ADJ_THREADS, 7) adj_kernel(const Ctx cx, const
   const Tile tl = tiles[blockIdx.y];
   pdl_trigger();
   {
-    // L2 prefetch of the first 1 KB of each of this CTA's factor columns
+    // L2 prefetch of the first 1 KB of each of this CTA's factor columns (a
+    // whole-tile prefetch on few-tile stages measured neutral on c1 / c4,
+    // profiles/r02_fwd_variants_ab.txt)
     const DevBlock &B = cx.blocks[tl.blk];
     const int t = threadIdx.x;
     const int col = tl.start + (t >> 3), line = t & 7;
@@ -1122,26 +1124,30 @@ template <bool ADJ>
 __host__ __device__ constexpr int ws_a_elems() {
   return ADJ ? MM_BM * 16 : 16 * (MM_BM + 2);
 }
-// B chunk: fragment order (BK x 32 slots)
-constexpr int WS_B_ELEMS = 16 * 32;
+// B chunk: fragment order (BK x 8 NT slots)
+template <int NT>
+__host__ __device__ constexpr int ws_b_elems() {
+  return 16 * 8 * NT;
+}
 
-template <bool ADJ>
+template <bool ADJ, int NT>
 __host__ __device__ constexpr int ws_smem_bytes() {
   // NS x (A tile + B chunk) operand buffers + 2 NS mbarriers + 1 KB to align
   // the stages to the 1024-byte period of the 128-byte TMA swizzle
-  return WS_STAGES * (ws_a_elems<ADJ>() + WS_B_ELEMS) * 16 + 2 * WS_STAGES * 8 + 1024;
+  return WS_STAGES * (ws_a_elems<ADJ>() + ws_b_elems<NT>()) * 16 + 2 * WS_STAGES * 8 + 1024;
 }
 
-// Complex plans, nrhs >= 32 (profiles/r01_mma_ws_ab.txt: c2 nrhs 32 forward
-// 18.1 vs 21.5 ms, adjoint 18.5 vs 19.9 ms against the classic structure).
-// Complex products by Gauss's 3-multiplication form.
-template <bool ADJ>
+// Complex plans, nrhs >= 16: 8 NT right-hand sides per CTA (NT = 4 for nrhs >=
+// 32, NT = 2 for 16..31) (profiles/r01_mma_ws_ab.txt: c2 nrhs 32 forward 18.1
+// vs 21.5 ms, adjoint 18.5 vs 19.9 ms against the classic structure; the
+// classic kernel's per-element forward gather ran the c5 stand-in's nrhs = 16
+// forward at 20 TF).  Complex products by Gauss's 3-multiplication form.
+template <bool ADJ, int NT>
 __global__ void __launch_bounds__(WS_THREADS, WS_MINB) mma_ws_kernel(const Ctx cx, const Tile *__restrict__ tiles,
                                                                      int from_f) {
   using S = double2;
   using X = Tr<S>;
   using PL = Planes<S>;
-  constexpr int NT = 4;
   constexpr bool M3 = true;
   constexpr int BK = mm_bk<S>();
   constexpr int KS = BK / 4;
@@ -1149,7 +1155,7 @@ __global__ void __launch_bounds__(WS_THREADS, WS_MINB) mma_ws_kernel(const Ctx c
   constexpr int A_CH = ws_a_elems<ADJ>();
   constexpr int AP = MM_BM + 2;  // forward tile leading dimension
   constexpr int MODE = ADJ ? 1 : 0;
-  constexpr int B_CH = WS_B_ELEMS;
+  constexpr int B_CH = ws_b_elems<NT>();
   constexpr int NS = WS_STAGES;
   extern __shared__ __align__(128) unsigned char ws_smem[];
   // stage buffers start at a 1024-byte boundary (shared-space address)
@@ -1162,7 +1168,7 @@ __global__ void __launch_bounds__(WS_THREADS, WS_MINB) mma_ws_kernel(const Ctx c
   pdl_trigger();
   const Tile tl = tiles[blockIdx.y];  // plan tables: never written by kernels
   const DevBlock B = cx.blocks[tl.blk];
-  const int rhs0 = blockIdx.x * 32;
+  const int rhs0 = blockIdx.x * 8 * NT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const S *T = static_cast<const S *>(cx.coef) + B.coef_off;
   const int64_t ld = B.ld;
@@ -1357,11 +1363,12 @@ void smem_optin(int bytes) {
   if (dev < 64) done |= 1ull << dev;
 }
 
-template <bool ADJ>
+template <bool ADJ, int NT>
 void mma_ws_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
-  constexpr int smem = ws_smem_bytes<ADJ>();
-  smem_optin<mma_ws_kernel<ADJ>>(smem);
-  launch_ex(PDL_MMA, mma_ws_kernel<ADJ>, dim3((cx.nrhs + 31) / 32, nt), dim3(WS_THREADS), smem, st, cx, tiles, from_f);
+  constexpr int smem = ws_smem_bytes<ADJ, NT>();
+  smem_optin<mma_ws_kernel<ADJ, NT>>(smem);
+  launch_ex(PDL_MMA, mma_ws_kernel<ADJ, NT>, dim3((cx.nrhs + 8 * NT - 1) / (8 * NT), nt), dim3(WS_THREADS), smem, st, cx,
+            tiles, from_f);
 }
 
 // ------------------------------------------------------------------------
@@ -1558,8 +1565,9 @@ void mma_real_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaS
 }
 
 // Multi-RHS dispatch: real plans at nrhs >= 32 -> mma_real_kernel; complex
-// plans at nrhs >= 32 -> mma_ws_kernel; narrower widths -> mma_kernel with 8 or
-// 16 right-hand sides per CTA (complex products in Gauss's 3-product form).
+// plans at nrhs >= 16 -> mma_ws_kernel (32 or 16 right-hand sides per CTA);
+// narrower widths -> mma_kernel with 8 or 16 right-hand sides per CTA (complex
+// products in Gauss's 3-product form).
 template <class S, bool ADJ, int NT>
 void mma_launch(const Ctx &cx, const Tile *tiles, int nt, int from_f, cudaStream_t st) {
   launch_ex(PDL_MMA, mma_kernel<S, ADJ, NT, true, 4>, dim3((cx.nrhs + 8 * NT - 1) / (8 * NT), nt), dim3(MM_THREADS), 0,
@@ -1572,11 +1580,14 @@ void mma_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cuda
     const int nt = ntiles - t0 < 65535 ? ntiles - t0 : 65535;
     if (cx.nrhs >= 32) {
       if constexpr (Planes<S>::cplx)
-        mma_ws_launch<ADJ>(cx, tiles + t0, nt, from_f, st);
+        mma_ws_launch<ADJ, 4>(cx, tiles + t0, nt, from_f, st);
       else
         mma_real_launch<ADJ>(cx, tiles + t0, nt, from_f, st);
     } else if (cx.nrhs >= 16) {
-      mma_launch<S, ADJ, 2>(cx, tiles + t0, nt, from_f, st);
+      if constexpr (Planes<S>::cplx)
+        mma_ws_launch<ADJ, 2>(cx, tiles + t0, nt, from_f, st);
+      else
+        mma_launch<S, ADJ, 2>(cx, tiles + t0, nt, from_f, st);
     } else {
       mma_launch<S, ADJ, 1>(cx, tiles + t0, nt, from_f, st);
     }
@@ -1780,8 +1791,7 @@ void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, 
     fwd_dispatch<double>(ctx, tiles, ntiles, latency, (cudaStream_t)stream);
 }
 
-void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
-                void *stream) {
+void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f, void *stream) {
   if (ntiles <= 0) return;
   if (is_complex)
     adj_dispatch<double2>(ctx, tiles, ntiles, in_from_f ? 1 : 0, (cudaStream_t)stream);
