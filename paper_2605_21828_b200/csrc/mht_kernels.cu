@@ -158,7 +158,9 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
 // adds them in split order — deterministic, no float atomics.
 // ------------------------------------------------------------------------
 // CG: workspace reads through L2 only (the persistent kernel; see in_value)
-template <class S, bool CG>
+// PFD: the L2 prefetch runs this many batch rounds ahead (8: c1 107.6 -> 105.0 us,
+// c4 81.4 -> 79.9 us against 2; profiles/r02_fwd_variants_ab.txt)
+template <class S, bool CG, int PFD = 8>
 __device__ __forceinline__ void fwd_tile_lat(const Ctx &cx, const Tile tl) {
   using X = Tr<S>;
   const DevBlock B = cx.blocks[tl.blk];
@@ -186,7 +188,7 @@ __device__ __forceinline__ void fwd_tile_lat(const Ctx &cx, const Tile tl) {
   // factor loads never wait behind an index -> value chain; the warps then
   // take batches of FB columns in turn (w, w + 4, ...: a tile's tail costs at
   // most one batch), all of a batch's loads issued before their first use,
-  // with an L2 prefetch of the warp's batch two ahead
+  // with an L2 prefetch of the warp's batch PFD rounds ahead
   constexpr int XCH = REAL ? 2048 : 1024;  // 16 KB
   constexpr int FB = REAL ? 8 : 4;
   __shared__ S xs[XCH];
@@ -204,8 +206,8 @@ __device__ __forceinline__ void fwd_tile_lat(const Ctx &cx, const Tile tl) {
     constexpr int JS = 4 * FB;
     const S *colc = T + (int64_t)jc * ld;
     for (int j = wb; j < we; j += JS) {
-      {  // L2 prefetch of the batch two ahead: column (lane >> 2), 128-byte lines (lane & 3) (+ 4)
-        const int jp = j + 2 * JS + (lane >> 2);
+      {  // L2 prefetch of the batch PFD rounds ahead: column (lane >> 2), 128-byte lines (lane & 3) (+ 4)
+        const int jp = j + PFD * JS + (lane >> 2);
         if (jp < we) {
           const char *pc = reinterpret_cast<const char *>(colc + (int64_t)jp * ld + tl.start);
           const int o = (lane & 3) * 128;
