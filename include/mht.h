@@ -21,8 +21,11 @@
  *    double (re, im) (flat square), MHT_DTYPE_F64 = double (sphere, meshes).
  *  - Vectors are column-major blocks: c is m x nrhs with leading dimension m
  *    (a contiguous (nrhs, m) array), f is n x nrhs with leading dimension n.
- *  - c is in the plan's frequency order (eigenvalue order); f is in the user's
- *    point order (the plan's perm_x maps tree order back to it).
+ *  - c is in the user's frequency order (eigenvalue order); f is in the user's
+ *    point order.  The plan's perm_x maps its space-tree order back to the
+ *    points; a version-2 plan's perm_k maps its frequency-tree order back to
+ *    the coefficients (the quadtree-frequency plans, reading A18),
+ *    fused into the loads / stores of c like perm_x into those of f.
  *  - Device-pointer calls (mht_apply, mht_apply_adjoint) enqueue on the plan's
  *    stream and return without synchronising; a device fault surfaces as
  *    MHT_ERR_CUDA on a later call or on mht_sync.
@@ -102,7 +105,7 @@ mht_status mht_reserve(mht_plan *plan, int nrhs);
 /* Synthesis f = Phi_BF c (Eq. MHT-sum, f_j = sum_k c_k
  * phi_k(x_j); evaluated through the factorization of §2, one
  * multiply per stored factor).  c: device, m x nrhs (ld m), in
- * the plan's frequency order; f: device, n x nrhs (ld n), user point order,
+ * the user's frequency order (perm_k, if any, applied on load); f: device, n x nrhs (ld n), user point order,
  * fully overwritten.  Runs the leaf projection, the L transfer stages and the
  * leaf interpolation (perm_x scatter fused into the store).  nrhs >= 1;
  * c and f must not overlap.  Errors: MHT_ERR_INVALID_ARG (null, nrhs < 1,
@@ -169,8 +172,8 @@ mht_status mht_apply_adjoint_shard_end(mht_plan *plan, void *c, int nrhs);
 /* ---- applications on top of the transform (§7) ----------------
  * A real diagonal on the coefficient side is fused into the transform's own
  * loads of c (synthesis) or its final stores of c (analysis): no extra pass
- * over c.  d / S: device float64 arrays of m entries in the plan's frequency
- * order; the same diagonal for every right-hand side.
+ * over c.  d / S: device float64 arrays of m entries in the order of c; the
+ * same diagonal for every right-hand side.
  *
  * Spectral filtering (§7.1):  f = Phi diag(F(lambda)) c. */
 mht_status mht_apply_diag(mht_plan *plan, const void *c, const double *d, void *f, int nrhs);

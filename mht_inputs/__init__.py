@@ -86,10 +86,9 @@ def flat_modes_kd(side: int, L: int) -> np.ndarray:
 
 
 def flat_workload_modes(w) -> np.ndarray:
-    """The mode list (c order) of a flat workload: eigenvalue order (reading A7/A8)
-    or, for extra["ftree"] == "kd", the 2-D kd (quadtree) frequency order."""
-    if w.extra.get("ftree") == "kd":
-        return flat_modes_kd(w.extra["side"], w.L)[: w.m]
+    """The mode list of a flat workload in the user's c order: eigenvalue order
+    (reading A7/A8).  (A quadtree-frequency plan factorizes in the kd order of
+    flat_modes_kd and maps it back with its perm_k; the user's order is this one.)"""
     return flat_modes(w.extra["side"])[: w.m]
 
 

@@ -272,6 +272,9 @@ int orc_dense_analysis(int64_t n, int64_t m, const double *Phi, int is_complex,
  *     i64 n, i64 m, i32 L, i32 0, f64 tol, i64 n_stages (= L+2),
  *     u64 checksum (wrapping sum of the body's u64 words), i64 body_bytes.
  *   body: i32 perm_x[n] (padded to 8 B); i64 sp_off[2^L+1]; i64 fr_off[2^L+1];
+ *     version 2 only: i32 perm_k[m] (padded to 8 B), plan frequency position ->
+ *     user coefficient index (reading A18: quadtree-frequency plans keep the
+ *     user's c order; c[perm_k[q]] is the plan's column q);
  *     then per stage s = 0..L+1: i64 s, i64 nblk, i64 nidx, i64 ncoef,
  *     scalar coef[ncoef] (8 or 16 B each),
  *     nblk x {i32 kind, i32 r_out, i32 r_in, i32 0, i64 idx_off, i64 coef_off},
@@ -299,6 +302,7 @@ typedef struct {
   double tol;
   const int32_t *perm;
   const int64_t *sp_off, *fr_off;
+  const int32_t *perm_k; /* NULL: the plan's frequency order is the user's */
   orc_stage *st; /* L + 2 */
 } orc_plan;
 
@@ -336,7 +340,8 @@ orc_plan *orc_plan_open(const char *path, int verify_checksum) {
   orc_plan *p = calloc(1, sizeof *p);
   p->map = map;
   p->map_bytes = bytes;
-  if (memcmp(h, "BFMHTPLN", 8) != 0 || *(const uint32_t *)(h + 8) != 1u) {
+  const uint32_t version = *(const uint32_t *)(h + 8);
+  if (memcmp(h, "BFMHTPLN", 8) != 0 || (version != 1u && version != 2u)) {
     snprintf(orc_err, sizeof orc_err, "bad magic/version");
     orc_plan_close(p);
     return NULL;
@@ -373,6 +378,11 @@ orc_plan *orc_plan_open(const char *path, int verify_checksum) {
   q += 8 * (nl + 1);
   p->fr_off = (const int64_t *)q;
   q += 8 * (nl + 1);
+  p->perm_k = NULL;
+  if (version == 2u) {
+    p->perm_k = (const int32_t *)q;
+    q += ((p->m * 4 + 7) / 8) * 8;
+  }
   p->st = calloc((size_t)nst, sizeof(orc_stage));
   size_t sc = p->dtype == 2 ? 16 : 8;
   for (int s = 0; s < nst; ++s) {
@@ -538,9 +548,15 @@ int orc_bf_apply(const orc_plan *P, const double *c, double *f, int64_t nrhs) {
   const int64_t nl = (int64_t)1 << L;
   int64_t *zoff_prev = malloc(sizeof(int64_t) * (size_t)(nl + 1));
   int64_t *zoff = malloc(sizeof(int64_t) * (size_t)(nl + 1));
+  double *cperm = P->perm_k ? malloc(sizeof(double) * cw * (size_t)P->m) : NULL;
   for (int64_t r = 0; r < nrhs; ++r) {
     const double *cr = c + (size_t)cw * (size_t)(r * P->m);
     double *fr = f + (size_t)cw * (size_t)(r * P->n);
+    if (P->perm_k) { /* the plan's column q is the user's coefficient perm_k[q] */
+      for (int64_t q = 0; q < P->m; ++q)
+        for (int k = 0; k < cw; ++k) cperm[cw * q + k] = cr[cw * (int64_t)P->perm_k[q] + k];
+      cr = cperm;
+    }
     /* level 0 */
     zoff_prev[0] = 0;
     for (int64_t v = 0; v < nl; ++v) zoff_prev[v + 1] = zoff_prev[v] + P->st[0].blk[v].r_out;
@@ -608,6 +624,7 @@ int orc_bf_apply(const orc_plan *P, const double *c, double *f, int64_t nrhs) {
     }
     free(zp);
   }
+  free(cperm);
   free(zoff_prev);
   free(zoff);
   return 0;
@@ -620,9 +637,11 @@ int orc_bf_adjoint(const orc_plan *P, const double *f, double *c, int64_t nrhs) 
   const int64_t nl = (int64_t)1 << L;
   int64_t *zoff = malloc(sizeof(int64_t) * (size_t)(nl + 1));
   int64_t *zoff_lo = malloc(sizeof(int64_t) * (size_t)(nl + 1));
+  double *cperm = P->perm_k ? malloc(sizeof(double) * cw * (size_t)P->m) : NULL;
   for (int64_t r = 0; r < nrhs; ++r) {
     const double *fr = f + (size_t)cw * (size_t)(r * P->n);
-    double *cr = c + (size_t)cw * (size_t)(r * P->m);
+    double *cuser = c + (size_t)cw * (size_t)(r * P->m);
+    double *cr = P->perm_k ? cperm : cuser; /* the plan's frequency order; scattered below */
     /* z_L(tau) = U_tau^* f(tau) */
     const orc_stage *SU = &P->st[L + 1];
     zoff[0] = 0;
@@ -679,7 +698,11 @@ int orc_bf_adjoint(const orc_plan *P, const double *f, double *c, int64_t nrhs) 
     for (int64_t v = 0; v < nl; ++v)
       orc_block_adjoint_add(P, &P->st[0], &P->st[0].blk[v], z + cw * zoff[v], cr + cw * P->fr_off[v]);
     free(z);
+    if (P->perm_k) /* the plan's column q is the user's coefficient perm_k[q] */
+      for (int64_t q = 0; q < P->m; ++q)
+        for (int k = 0; k < cw; ++k) cuser[cw * (int64_t)P->perm_k[q] + k] = cperm[cw * q + k];
   }
+  free(cperm);
   free(zoff);
   free(zoff_lo);
   return 0;

@@ -77,6 +77,7 @@ struct Ctx {  // per-launch pointers
   const void *coef;
   const int32_t *idx;
   const int32_t *perm;
+  const int32_t *permk;  // plan frequency position -> user c index (plan v2), nullptr = identity
   const DevBlock *blocks;
   const void *c;   // SRC_C base
   void *cw;        // writable c (adjoint output)

@@ -126,6 +126,11 @@ struct Tr<double2> {
 // Coefficient-side diagonal (spectral filter F(lambda_k), GRF sqrt S(lambda_k),
 // covariance S; §7.1, §7.2), fused into the
 // loads of c (forward) and the stores of c (adjoint).
+// c is read and written in the user's order: the plan's frequency position q
+// is the user's coefficient perm_k[q] (plan v2, quadtree-frequency plans,
+// reading A18); without perm_k the orders agree
+__device__ __forceinline__ int64_t user_c_index(const Ctx &cx, int64_t q) { return cx.permk ? cx.permk[q] : q; }
+// (the diagonal is indexed like c: user order)
 __device__ __forceinline__ double diag_at(const Ctx &cx, int64_t k) {
   const double d = cx.diag[k];
   return cx.diag_sqrt ? sqrt(d) : d;
@@ -140,9 +145,10 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
   const bool s1 = q >= B.seg_len[0];  // no dynamic indexing: keeps B in registers
   const int64_t off = s1 ? B.seg_off[1] + (q - B.seg_len[0]) : B.seg_off[0] + q;
   const int32_t src = s1 ? B.seg_src[1] : B.seg_src[0];
-  if (src == SRC_C) {  // user layout: column-major
-    const S v = static_cast<const S *>(cx.c)[r * cx.m + off];
-    return cx.diag ? Tr<S>::scale(v, diag_at(cx, off)) : v;
+  if (src == SRC_C) {  // user layout: column-major, user order (plan position -> user index by perm_k)
+    const int64_t ci = user_c_index(cx, off);
+    const S v = static_cast<const S *>(cx.c)[r * cx.m + ci];
+    return cx.diag ? Tr<S>::scale(v, diag_at(cx, ci)) : v;
   }
   const S *p = static_cast<const S *>(cx.z) + off * cx.nrhs + r;           // workspace: RHS-fastest
   if constexpr (CG) return Tr<S>::ldcg(p);
@@ -1277,7 +1283,7 @@ __global__ void __launch_bounds__(WS_THREADS, WS_MINB) mma_ws_kernel(const Ctx c
             const bool s1 = qq >= B.seg_len[0];
             const int64_t off = s1 ? B.seg_off[1] + (qq - B.seg_len[0]) : B.seg_off[0] + qq;
             if ((s1 ? B.seg_src[1] : B.seg_src[0]) == SRC_C) {
-              rb[k4] = static_cast<const S *>(cx.c) + off;
+              rb[k4] = static_cast<const S *>(cx.c) + user_c_index(cx, off);
               rs[k4] = cx.m;
             } else {
               rb[k4] = static_cast<const S *>(cx.z) + off * cx.nrhs;
@@ -1477,7 +1483,7 @@ __global__ void __launch_bounds__(MM_THREADS, MINB) mma_real_kernel(const Ctx cx
         const bool s1 = qr >= B.seg_len[0];
         const int64_t off = s1 ? B.seg_off[1] + (qr - B.seg_len[0]) : B.seg_off[0] + qr;
         if ((s1 ? B.seg_src[1] : B.seg_src[0]) == SRC_C) {
-          srow = static_cast<const S *>(cx.c) + (int64_t)rhs0 * cx.m + off;
+          srow = static_cast<const S *>(cx.c) + (int64_t)rhs0 * cx.m + user_c_index(cx, off);
           rstride = cx.m;
         } else {
           srow = static_cast<const S *>(cx.z) + off * cx.nrhs + rhs0;
@@ -1614,8 +1620,10 @@ __device__ __forceinline__ void reduce_piece(const Ctx &cx, const Piece p, const
       const S *a = part + (rd[p.rd_begin + q] + i) * nr + r;
       s = X::add(s, CG ? X::ldcg(a) : *a);
     }
-    if (p.dst_src == SRC_C)
-      static_cast<S *>(cx.cw)[r * cx.m + p.dst_off + i] = cx.diag ? X::scale(s, diag_at(cx, p.dst_off + i)) : s;
+    if (p.dst_src == SRC_C) {
+      const int64_t ci = user_c_index(cx, p.dst_off + i);
+      static_cast<S *>(cx.cw)[r * cx.m + ci] = cx.diag ? X::scale(s, diag_at(cx, ci)) : s;
+    }
     else
       static_cast<S *>(cx.z)[(p.dst_off + i) * nr + r] = s;
   }

@@ -104,6 +104,7 @@ struct mht_plan {
   void *d_coef = nullptr;
   int32_t *d_idx = nullptr;
   int32_t *d_perm = nullptr;
+  int32_t *d_permk = nullptr;  // plan v2 frequency permutation (nullptr: none)
   DevBlock *d_blocks = nullptr;
   Tile *d_fwd = nullptr;   // 64-row tiles (multi-RHS DMMA path)
   Tile *d_fwd1 = nullptr;  // nrhs = 1 tiles, with column splits on low-parallelism stages
@@ -179,7 +180,7 @@ struct mht_plan {
     for (void *p : lsqr_buf)
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
-    for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_blocks, (void *)d_fwd, (void *)d_fwd1, d_fsplit, (void *)d_fcount,
+    for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_permk, (void *)d_blocks, (void *)d_fwd, (void *)d_fwd1, d_fsplit, (void *)d_fcount,
                     (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, (void *)d_phases, (void *)d_ctr, (void *)d_stamps, d_msplit, (void *)d_mcount, d_ctmp, d_tmaps, d_z, d_part, d_hc, d_hf})
       if (p) cudaFree(p);
   }
@@ -264,7 +265,7 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
   memcpy(&nst, hdr + 48, 8);
   memcpy(&csum, hdr + 56, 8);
   memcpy(&body, hdr + 64, 8);
-  if (ver != 1) return fail(MHT_ERR_FORMAT, "unsupported plan version");
+  if (ver != 1 && ver != 2) return fail(MHT_ERR_FORMAT, "unsupported plan version");
   if (dt != 1 && dt != 2) return fail(MHT_ERR_FORMAT, "bad dtype");
   if (L < 0 || L > 24 || nst != L + 2) return fail(MHT_ERR_FORMAT, "bad L / stage count");
   if (body < 0 || body + 256 != fbytes) return fail(MHT_ERR_FORMAT, "body size mismatch");
@@ -281,6 +282,18 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
       !R.read(fr_off.data(), 8 * (nl + 1)))
     return fail(MHT_ERR_FORMAT, "truncated trees");
   perm.resize(P->n);
+  // version 2: the frequency permutation perm_k (plan position -> user c index)
+  std::vector<int32_t> perm_k;
+  if (ver == 2) {
+    perm_k.resize(pad8(4 * P->m) / 4);
+    if (!R.read(perm_k.data(), pad8(4 * P->m))) return fail(MHT_ERR_FORMAT, "truncated perm_k");
+    perm_k.resize(P->m);
+    std::vector<char> seen(P->m, 0);
+    for (int32_t j : perm_k) {
+      if (j < 0 || j >= P->m || seen[j]) return fail(MHT_ERR_FORMAT, "perm_k is not a permutation");
+      seen[j] = 1;
+    }
+  }
   if (sp_off[0] != 0 || sp_off[nl] != P->n || fr_off[0] != 0 || fr_off[nl] != P->m)
     return fail(MHT_ERR_FORMAT, "tree offsets do not cover n / m");
   for (int64_t i = 0; i < nl; ++i)
@@ -1079,6 +1092,7 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
   mht_status st;
   if ((st = upload(&P->d_idx, idx_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_perm, perm, P->device_bytes)) != MHT_OK) return st;
+  if (!perm_k.empty() && (st = upload(&P->d_permk, perm_k, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_blocks, blocks, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_fwd, fwd_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_fwd1, fwd1_all, P->device_bytes)) != MHT_OK) return st;
@@ -1139,6 +1153,7 @@ Ctx make_ctx(mht_plan *P, int nrhs) {
   cx.coef = P->d_coef;
   cx.idx = P->d_idx;
   cx.perm = P->d_perm;
+  cx.permk = P->d_permk;
   cx.blocks = P->d_blocks;
   cx.z = P->d_z;
   cx.part = P->d_part;

@@ -54,13 +54,13 @@ def _job(task):
     return b, KIND_ID, k, c, skel, red, T, Jin[skel]
 
 
-def build_plan(basis, perm, sp_off, fr_off, L, tol, path, workers=None, log=print, seed=1234):
+def build_plan(basis, perm, sp_off, fr_off, L, tol, path, workers=None, log=print, seed=1234, perm_k=None):
     """Factorize Phi (given by ``basis.block(rows, cols)``) and stream the plan
     to ``path``.  Returns a dict of statistics."""
     n, m = basis.n, basis.m
     nl = 1 << L
     workers = workers or max(1, os.cpu_count() or 1)
-    w = PlanWriter(path, basis.dtype, n, m, L, tol, perm, sp_off, fr_off)
+    w = PlanWriter(path, basis.dtype, n, m, L, tol, perm, sp_off, fr_off, perm_k=perm_k)
     all_rows = np.asarray(perm, dtype=np.int64)
     stats = {"stages": [], "n": n, "m": m, "L": L, "tol": tol}
     ctx = mp.get_context("fork")

@@ -193,12 +193,12 @@ def _chunks(nblk_rows, nblk_cols, budget_elems):
 
 
 def build_plan_gpu(basis, perm, sp_off, fr_off, L, tol, path, device="cuda", log=print, seed=1234,
-                   budget_gb=3.0):
+                   budget_gb=3.0, perm_k=None):
     import torch
 
     n, m = basis.n, basis.m
     nl = 1 << L
-    w = PlanWriter(path, basis.dtype, n, m, L, tol, perm, sp_off, fr_off)
+    w = PlanWriter(path, basis.dtype, n, m, L, tol, perm, sp_off, fr_off, perm_k=perm_k)
     perm_np = np.asarray(perm, np.int64)
     esz = 16 if basis.dtype == np.complex128 else 8
     budget = int(budget_gb * 1e9 / esz)

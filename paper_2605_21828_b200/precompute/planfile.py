@@ -5,7 +5,7 @@ Layout (little-endian; DESIGN.md §4 is the normative description):
 header, 256 bytes::
 
     0   char[8]  "BFMHTPLN"
-    8   u32      version = 1
+    8   u32      version = 1, or 2 when the plan carries a frequency permutation
     12  u32      dtype   (1 = float64, 2 = complex128)
     16  i64      n       (spatial points, rows of Phi)
     24  i64      m       (eigenfunctions, columns of Phi)
@@ -21,7 +21,10 @@ body::
 
     i32 perm_x[n]           tree position -> user point index (pad to 8 B)
     i64 sp_off[2^L + 1]     space-leaf row offsets (in tree positions)
-    i64 fr_off[2^L + 1]     frequency-leaf column offsets (c order)
+    i64 fr_off[2^L + 1]     frequency-leaf column offsets (plan frequency order)
+    i32 perm_k[m]           (version 2 only) plan frequency position -> user coefficient index,
+                            pad to 8 B: c[perm_k[q]] feeds plan column q (the quadtree-frequency
+                            plans keep the user's eigenvalue order of c, reading A18)
     stage s = 0 .. L+1:
         i64 s, i64 nblk (= 2^L), i64 nidx, i64 ncoef
         scalar coef[ncoef]                   (8 B real / 16 B complex)
@@ -53,7 +56,8 @@ from dataclasses import dataclass
 import numpy as np
 
 MAGIC = b"BFMHTPLN"
-VERSION = 1
+VERSION = 1           # without a frequency permutation
+VERSION_PERMK = 2     # with perm_k[m] after fr_off
 HEADER_BYTES = 256
 KIND_IDENTITY, KIND_ID, KIND_DENSE = 0, 1, 2
 DT_REAL, DT_COMPLEX = 1, 2
@@ -82,7 +86,7 @@ class PlanWriter:
         w.close()
     """
 
-    def __init__(self, path, dtype, n, m, L, tol, perm, sp_off, fr_off):
+    def __init__(self, path, dtype, n, m, L, tol, perm, sp_off, fr_off, perm_k=None):
         self.path = str(path)
         self.complex = np.dtype(dtype) == np.complex128
         self.sdt = np.dtype("<c16") if self.complex else np.dtype("<f8")
@@ -101,6 +105,12 @@ class PlanWriter:
         self._write(_pad8(perm.tobytes()))
         self._write(sp_off.tobytes())
         self._write(fr_off.tobytes())
+        self.version = VERSION
+        if perm_k is not None:
+            perm_k = np.asarray(perm_k, dtype="<i4")
+            assert perm_k.shape == (self.m,) and np.array_equal(np.sort(perm_k), np.arange(self.m))
+            self._write(_pad8(perm_k.tobytes()))
+            self.version = VERSION_PERMK
         self.stage = None
         self.entries = 0
         self.stage_stats = []
@@ -217,7 +227,7 @@ class PlanWriter:
         assert self.stage is None
         self.f.seek(0)
         hdr = bytearray(HEADER_BYTES)
-        struct.pack_into("<8sIIqqiidqQq", hdr, 0, MAGIC, VERSION,
+        struct.pack_into("<8sIIqqiidqQq", hdr, 0, MAGIC, self.version,
                          DT_COMPLEX if self.complex else DT_REAL, self.n, self.m, self.L, 0,
                          self.tol, self.L + 2, self.csum, self.body)
         self.f.write(bytes(hdr))
@@ -244,8 +254,8 @@ class PlanView:
         self.mm = np.memmap(self.path, dtype=np.uint8, mode="r")
         h = bytes(self.mm[:HEADER_BYTES])
         (magic, ver, dt, n, m, L, _z, tol, nst, csum, body) = struct.unpack_from("<8sIIqqiidqQq", h, 0)
-        if magic != MAGIC or ver != VERSION:
-            raise ValueError("not a v1 plan")
+        if magic != MAGIC or ver not in (VERSION, VERSION_PERMK):
+            raise ValueError("not a v1 / v2 plan")
         self.complex = dt == DT_COMPLEX
         self.sdt = np.dtype("<c16") if self.complex else np.dtype("<f8")
         self.n, self.m, self.L, self.tol, self.checksum, self.body = n, m, L, tol, csum, body
@@ -257,6 +267,10 @@ class PlanView:
         q += 8 * (nl + 1)
         self.fr_off = self.mm[q:q + 8 * (nl + 1)].view("<i8")
         q += 8 * (nl + 1)
+        self.perm_k = None
+        if ver == VERSION_PERMK:
+            self.perm_k = self.mm[q:q + 4 * m].view("<i4")
+            q += ((4 * m + 7) // 8) * 8
         self.stages = []
         for s in range(L + 2):
             sh = self.mm[q:q + 32].view("<i8")

@@ -81,7 +81,7 @@ class ClosedFormBands:
 
 
 def build_plan_streaming(bands, perm, sp_off, fr_off, L, tol, path, seed=1234, workers=None, log=print,
-                         spool_dir=None):
+                         spool_dir=None, perm_k=None):
     """Alg. 3: post-order streaming factorization of Phi, whose columns come
     from ``bands(c0, c1)`` (n x (c1 - c0), rows in user point order), one
     frequency leaf at a time.  Writes the v1 plan to ``path``; returns stats
@@ -199,7 +199,7 @@ def build_plan_streaming(bands, perm, sp_off, fr_off, L, tol, path, seed=1234, w
             f.close()
     # ---- assemble the plan in stage order from the spools
     try:
-        w = PlanWriter(path, dtype, n, m, L, tol, perm, sp_off, fr_off)
+        w = PlanWriter(path, dtype, n, m, L, tol, perm, sp_off, fr_off, perm_k=perm_k)
         for s in range(L + 2):
             idx, nidx, rows = [], 0, []
             for (kind, r_out, r_in, skel, red, off) in recs[s]:
@@ -297,7 +297,7 @@ def _main():
             Phi = bf(0, w.m).copy()
             st = build_plan(DenseBasis(Phi), perm, sp_off, fr_off, w.L, w.tol, out, workers=1, log=None)
     else:
-        basis, perm, sp_off, fr_off = W.setup(w)
+        basis, perm, sp_off, fr_off, _ = W.setup(w)
         rss0 = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss
         t1 = time.time()
         pk = _Peak()

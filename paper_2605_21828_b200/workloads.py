@@ -26,11 +26,29 @@ def sphere_workload(n: int, lmax: int, L: int, tol: float, name: str = "sphere")
     return mi.Workload(name, "sphere", n, (lmax + 1) ** 2, "float64", tol, L, (1,), {"lmax": lmax})
 
 
+def freq_plan_order(w: mi.Workload):
+    """(plan mode list, perm_k) of a flat workload.  The user's c is in
+    eigenvalue order (mht_inputs.flat_workload_modes).  The quadtree-frequency
+    variant (extra["ftree"] == "kd", reading A18) factorizes the columns in the
+    2-D kd order of the frequency box and stores perm_k (plan position -> user
+    index) in the plan, so the library reads and writes c in the user's order;
+    otherwise the plan order is the user's order and there is no perm_k."""
+    k_user = mi.flat_workload_modes(w)
+    if w.extra.get("ftree") != "kd":
+        return k_user, None
+    k_plan = mi.flat_modes_kd(w.extra["side"], w.L)[: w.m]
+    idx = {tuple(v): i for i, v in enumerate(k_user.tolist())}
+    perm_k = np.array([idx[tuple(v)] for v in k_plan.tolist()], dtype=np.int32)
+    return k_plan, perm_k
+
+
 def setup(w: mi.Workload):
-    """Return (basis, perm, sp_off, fr_off)."""
+    """Return (basis, perm, sp_off, fr_off, perm_k); perm_k is None unless the
+    plan's frequency order differs from the user's (freq_plan_order)."""
+    perm_k = None
     if w.family == "flat":
         x = mi.flat_points(w.n, seed=w.extra.get("seed", mi.SEED_GEOMETRY))
-        k = mi.flat_workload_modes(w)
+        k, perm_k = freq_plan_order(w)
         basis = FlatBasis(x, k)
         perm, sp_off = kd_tree(x, w.L, alternate=True)
     elif w.family == "sphere":
@@ -44,14 +62,14 @@ def setup(w: mi.Workload):
     else:
         raise ValueError(w.family)
     fr_off = freq_tree(w.m, w.L)
-    return basis, perm, sp_off, fr_off
+    return basis, perm, sp_off, fr_off, perm_k
 
 
 def build_workload_plan(w: mi.Workload, path: str, workers=None, log=print, precompute_sphere=None,
                         builder: str = "cpu", device="cuda"):
     """builder = "cpu" (numpy/scipy CPQR, multiprocess) or "gpu" (batched
     torch CPQR on the device; same factorization, same file format)."""
-    basis, perm, sp_off, fr_off = setup(w)
+    basis, perm, sp_off, fr_off, perm_k = setup(w)
     if builder == "gpu":
         from .precompute import gpu_builder as G
 
@@ -64,16 +82,17 @@ def build_workload_plan(w: mi.Workload, path: str, workers=None, log=print, prec
 
             tb = G.TorchTableBasis(torch.as_tensor(np.asarray(basis.Phi), device=device), basis.dtype)
         try:
-            return G.build_plan_gpu(tb, perm, sp_off, fr_off, w.L, w.tol, path, device=device, log=log)
+            return G.build_plan_gpu(tb, perm, sp_off, fr_off, w.L, w.tol, path, device=device, log=log,
+                                    perm_k=perm_k)
         finally:
             del tb
     if isinstance(basis, SphereBasis) and (precompute_sphere or (precompute_sphere is None and w.n * w.m <= 6e9)):
         basis.precompute_all()
-    return build_plan(basis, perm, sp_off, fr_off, w.L, w.tol, path, workers=workers, log=log)
+    return build_plan(basis, perm, sp_off, fr_off, w.L, w.tol, path, workers=workers, log=log, perm_k=perm_k)
 
 
 # bump when the builders' numerics change so cached plans are never reused across versions
-BUILDER_VERSION = 4
+BUILDER_VERSION = 5  # 5: quadtree-frequency plans carry perm_k (plan v2)
 
 
 def plan_cache_path(w: mi.Workload, root: str | None = None) -> str:

@@ -131,6 +131,40 @@ def test_config1_quadtree_frequency_variant(gpu, oracle_lib, plans):
     check_plan(gpu, oracle_lib, path, w, (1, 4, 32), dense=flat_dense(oracle_lib, w))
 
 
+def test_frequency_permutation_plan_paths(gpu, oracle_lib, plans):
+    """A version-2 plan (perm_k: the quadtree-frequency order, c in the user's
+    eigenvalue order, reading A18) through every path that reads or writes c:
+    the nrhs = 1 kernels (per stage and one-launch), the classic and
+    warp-specialised DMMA kernels, the fused spectral filter on both sides and a
+    2-way sharded emulation; all vs O2 element by element and vs the dense sum."""
+    from paper_2605_21828_b200 import shard as SH
+
+    w = mi.Workload("kdperm", "flat", 2048, 1024, "complex128", 1e-8, 4, (1,), {"side": 32, "ftree": "kd"})
+    path = str(plans / "kdperm.plan")
+    W.build_workload_plan(w, path, workers=8, log=None)
+    P, O = check_plan(gpu, oracle_lib, path, w, (1, 5, 16, 33), dense=flat_dense(oracle_lib, w))
+    c, y = mi.complex_gaussian(3, w.m, 7), mi.complex_gaussian(3, w.n, 8)
+    ct, yt = torch.from_numpy(c).cuda(), torch.from_numpy(y).cuda()
+    P.set_persistent(True)
+    assert o2_err(P.apply(ct[:1]).cpu().numpy(), O.apply(c[:1])) <= PARITY
+    assert o2_err(P.adjoint(yt[:1]).cpu().numpy(), O.adjoint(y[:1])) <= PARITY
+    P.set_persistent(False)
+    F = np.linspace(0.5, 2.0, w.m)
+    Ft = torch.from_numpy(F).cuda()
+    assert o2_err(P.apply_diag(ct, Ft).cpu().numpy(), O.apply(c * F[None, :])) <= PARITY
+    assert o2_err(P.adjoint_diag(yt, Ft).cpu().numpy(), O.adjoint(y) * F[None, :]) <= PARITY
+    P.close()
+    shards = [SH.ShardPlan(path, 2, g, 0, -1) for g in range(2)]
+    f = torch.zeros((3, w.n), dtype=torch.complex128, device="cuda")
+    a = torch.zeros((3, w.m), dtype=torch.complex128, device="cuda")
+    SH.emulate_apply(shards, ct, f)
+    SH.emulate_adjoint(shards, yt, a)
+    assert o2_err(f.cpu().numpy(), O.apply(c)) <= PARITY
+    assert o2_err(a.cpu().numpy(), O.adjoint(y)) <= PARITY
+    for sh in shards:
+        sh.close()
+
+
 def test_sphere_parity(gpu, oracle_lib, plans):
     lmax = 31
     w = W.sphere_workload(2048, lmax, 4, 1e-10)

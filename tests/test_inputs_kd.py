@@ -30,8 +30,47 @@ def test_kd_modes_are_boxes(side, L):
 
 
 def test_kd_workloads_registered():
+    from paper_2605_21828_b200 import workloads as W
+
     for name, base in (("c1kd", "c1"), ("c2kd", "c2")):
         w, b = mi.WORKLOADS[name], mi.WORKLOADS[base]
         assert (w.n, w.m, w.L, w.tol, w.dtype) == (b.n, b.m, b.L, b.tol, b.dtype)
-        k = mi.flat_workload_modes(w)
-        assert k.shape == (w.m, 2) and not np.array_equal(k, mi.flat_workload_modes(b))
+        # the user's c order is the same eigenvalue order; the plan's is the kd order
+        assert np.array_equal(mi.flat_workload_modes(w), mi.flat_workload_modes(b))
+        k_plan, perm_k = W.freq_plan_order(w)
+        assert np.array_equal(k_plan, mi.flat_workload_modes(w)[perm_k])
+        assert W.freq_plan_order(b)[1] is None
+
+
+def test_plan_frequency_permutation_oracle(tmp_path, oracle_lib):
+    """Plan v2 (perm_k, reading A18): the oracle's O2 on a quadtree-frequency
+    plan with c in the user's eigenvalue order equals, bitwise, O2 on the same
+    factorization written without perm_k (v1) applied to c[perm_k] — synthesis
+    and analysis — and matches the dense sum with the eigenvalue-order modes."""
+    from paper_2605_21828_b200 import workloads as W
+    from paper_2605_21828_b200.precompute import build_plan
+    from paper_2605_21828_b200.precompute.basis import FlatBasis
+    from paper_2605_21828_b200.precompute.trees import freq_tree, kd_tree
+
+    w = mi.Workload("kdsmall", "flat", 1024, 1024, "complex128", 1e-8, 4, (1,), {"side": 32, "ftree": "kd"})
+    p2 = str(tmp_path / "kd_v2.plan")
+    W.build_workload_plan(w, p2, workers=2, log=None)
+    x = mi.flat_points(w.n)
+    k_plan, perm_k = W.freq_plan_order(w)
+    perm, sp_off = kd_tree(x, w.L, alternate=True)
+    p1 = str(tmp_path / "kd_v1.plan")
+    build_plan(FlatBasis(x, k_plan), perm, sp_off, freq_tree(w.m, w.L), w.L, w.tol, p1, workers=2, log=None)
+    O2, O1 = oracle_lib.Plan(p2), oracle_lib.Plan(p1)
+    c = mi.complex_gaussian(3, w.m, 1)
+    y = mi.complex_gaussian(3, w.n, 2)
+    assert np.array_equal(O2.apply(c), O1.apply(c[:, perm_k]))
+    a1 = O1.adjoint(y)
+    a2 = np.empty_like(a1)
+    a2[:, perm_k] = a1
+    assert np.array_equal(O2.adjoint(y), a2)
+    k_user = mi.flat_workload_modes(w)
+    fd, cd = oracle_lib.flat_synth(x, k_user, c), oracle_lib.flat_analysis(x, k_user, y)
+    f, ca = O2.apply(c), O2.adjoint(y)
+    for r in range(3):
+        assert np.linalg.norm(f[r] - fd[r]) / np.linalg.norm(fd[r]) <= 10 * w.tol
+        assert np.linalg.norm(ca[r] - cd[r]) / np.linalg.norm(cd[r]) <= 10 * w.tol
