@@ -1,9 +1,14 @@
-"""Device-accelerated plan builder (host precompute run on the GPU through torch).
+"""Device plan builder (host precompute, outside the timed path).
 
 Same factorization as ``builder.build_plan`` (§2), same
 plan file, but the block evaluation and the interpolative decompositions run
 batched on the GPU so the configs[1]/[2] plans (65,536^2, tens of GB) build in
-minutes instead of hours.  Outside the timed path; the hot path never calls it.
+minutes instead of hours.  The steps run in libmht's construction kernels
+(include/mht_build.h, csrc/mht_build.cu): Phi blocks evaluated in-kernel
+(flat) or gathered from an in-kernel harmonics table (sphere) / the stored
+eigenvectors (mesh), and the batched column-pivoted QR.  torch provides the
+device memory, the Gaussian sketches and the library GEMM / eigvalsh /
+triangular solve; this module arranges the batches and writes the file.
 
 Per stage, blocks are processed in canonical order in chunks of equal-shape
 batches (zero-padded: zero rows leave a column ID unchanged, zero columns are
@@ -25,6 +30,7 @@ import time
 
 import numpy as np
 
+from . import devkern
 from .planfile import KIND_DENSE, KIND_ID, KIND_IDENTITY, PlanWriter
 from .trees import node_rows
 
@@ -32,13 +38,16 @@ OVERSAMPLE = 16
 
 
 # ------------------------------------------------------------------ bases
-class TorchFlatBasis:
+class DeviceFlatBasis:
+    """Flat-square basis on the device; blocks evaluated in-kernel
+    (``mhtb_flat_blocks``, csrc/mht_build.cu)."""
+
     def __init__(self, x, k, device):
         import torch
 
         self.torch = torch
-        self.x = torch.as_tensor(np.asarray(x, np.float64), device=device)
-        self.k = torch.as_tensor(np.asarray(k, np.float64), device=device)
+        self.x = torch.as_tensor(np.ascontiguousarray(x, np.float64), device=device)
+        self.k = torch.as_tensor(np.ascontiguousarray(k, np.float64), device=device)
         self.n, self.m = self.x.shape[0], self.k.shape[0]
         self.dtype = np.complex128
         self.tdtype = torch.complex128
@@ -46,18 +55,12 @@ class TorchFlatBasis:
     def block_t(self, rows, cols):
         """rows (B,R) long (-1 = zero row), cols (B,C) long (-1 = zero column)
         -> At (B, C, R) with At[b, c, r] = Phi(rows[b,r], cols[b,c])."""
-        t = self.torch
-        kk = self.k[cols.clamp(min=0)]                     # (B, C, 2)
-        xx = self.x[rows.clamp(min=0)]                     # (B, R, 2)
-        ph = t.bmm(kk, xx.transpose(1, 2))                 # (B, C, R)
-        A = t.complex(t.cos(ph), t.sin(ph))
-        A.mul_(((cols >= 0)[:, :, None] & (rows >= 0)[:, None, :]).to(A.real.dtype))
-        return A
+        return devkern.flat_blocks(self.x, self.k, rows.contiguous(), cols.contiguous())
 
 
-class TorchTableBasis:
+class DeviceTableBasis:
     """Phi held on the device as a dense (n, m) table (sphere harmonics
-    evaluated once on the GPU, or stored mesh eigenvectors)."""
+    evaluated once in-kernel by ``sphere_table``, or stored mesh eigenvectors)."""
 
     def __init__(self, table, dtype):
         self.table = table  # torch (n, m)
@@ -73,106 +76,29 @@ class TorchTableBasis:
         c = cols.clamp(min=0)
         A = self.table[r[:, None, :].expand(B, C, R), c[:, :, None].expand(B, C, R)]
         mask = ((cols >= 0)[:, :, None] & (rows >= 0)[:, None, :])
-        return A * mask.to(A.dtype)
+        return (A * mask.to(A.dtype)).contiguous()
 
 
-def sphere_table_torch(theta, phi, lmax, device, chunk=4096):
+def sphere_table(theta, phi, lmax, device):
     """Real orthonormal SH (reading A11) at all points, (n, (lmax+1)^2) float64,
-    by the normalised associated-Legendre recurrence vectorised on the GPU."""
+    by the normalised associated-Legendre recurrence in-kernel
+    (``mhtb_sphere_table``)."""
     import torch
 
-    th = torch.as_tensor(np.asarray(theta, np.float64), device=device)
-    ph = torch.as_tensor(np.asarray(phi, np.float64), device=device)
-    n = th.shape[0]
-    M = (lmax + 1) ** 2
-    out = torch.empty((n, M), dtype=torch.float64, device=device)
-    ls = np.repeat(np.arange(lmax + 1), 2 * np.arange(lmax + 1) + 1)
-    ms = np.arange(M) - ls * ls - ls
-    am = torch.as_tensor(np.abs(ms), device=device)
-    lt = torch.as_tensor(ls, device=device)
-    # float64 from numpy: torch.where on two Python scalars would produce float32 (sqrt 2 to 1e-8)
-    scale = torch.as_tensor(np.where(ms == 0, 1.0, math.sqrt(2.0)).astype(np.float64), device=device)
-    pos = torch.as_tensor(ms >= 0, device=device)
-    mvec = torch.arange(lmax + 1, dtype=torch.float64, device=device)
-    for s in range(0, n, chunk):
-        x = torch.cos(th[s:s + chunk])
-        sn = torch.sin(th[s:s + chunk])
-        npt = x.shape[0]
-        P = torch.zeros((lmax + 1, lmax + 1, npt), dtype=torch.float64, device=device)
-        P[0, 0] = 1.0 / math.sqrt(4.0 * math.pi)
-        for mm in range(1, lmax + 1):
-            P[mm, mm] = math.sqrt((2.0 * mm + 1.0) / (2.0 * mm)) * sn * P[mm - 1, mm - 1]
-        for l in range(1, lmax + 1):
-            P[l, l - 1] = math.sqrt(2.0 * (l - 1) + 3.0) * x * P[l - 1, l - 1]
-            if l >= 2:
-                m_ = mvec[: l - 1]
-                a = torch.sqrt((4.0 * l * l - 1.0) / (l * l - m_ * m_))
-                b = torch.sqrt(((l - 1.0) ** 2 - m_ * m_) / (4.0 * (l - 1.0) ** 2 - 1.0))
-                P[l, : l - 1] = a[:, None] * (x[None, :] * P[l - 1, : l - 1] - b[:, None] * P[l - 2, : l - 1])
-        val = P[lt, am, :].T                                              # (npt, M)
-        mph = ph[s:s + chunk, None] * am[None, :].to(torch.float64)
-        trig = torch.where(pos[None, :], torch.cos(mph), torch.sin(mph))
-        out[s:s + npt] = val * scale[None, :] * trig
-        del P
-    return out
+    th = torch.as_tensor(np.ascontiguousarray(theta, np.float64), device=device)
+    ph = torch.as_tensor(np.ascontiguousarray(phi, np.float64), device=device)
+    return devkern.sphere_table(th, ph, lmax)
 
 
 # ------------------------------------------------------------------ CPQR
 def cpqr_batched(At, tol):
-    """In-place batched Householder QR with column pivoting of A = At^T.
+    """In-place batched Householder QR with column pivoting of A = At^T on the
+    device (``mhtb_cpqr``: one CTA per block).
 
-    At: (B, C, R) (column-contiguous).  Returns (ranks (B,), perm (B, C)); on
-    return At[b, c, r] = R_b[r, c] for r <= c (the upper-triangular factor of
-    A_b[:, perm_b])."""
-    import torch
-
-    B, C, R = At.shape
-    kmax = min(R, C)
-    dev = At.device
-    bidx = torch.arange(B, device=dev)
-    perm = torch.arange(C, device=dev).repeat(B, 1)
-    norms = (At.real ** 2 + (At.imag ** 2 if At.is_complex() else 0)).sum(-1)
-    r00 = norms.max(1).values.sqrt()
-    ranks = torch.full((B,), kmax, dtype=torch.long, device=dev)
-    done = torch.zeros(B, dtype=torch.bool, device=dev)
-    for j in range(kmax):
-        p = norms[:, j:].argmax(1) + j
-        rowp = At[bidx, p].clone()
-        At[bidx, p] = At[:, j].clone()  # (clone: p == j aliases the source)
-        At[:, j] = rowp
-        np_ = norms[bidx, p].clone()
-        norms[bidx, p] = norms[:, j].clone()
-        norms[:, j] = np_
-        pp = perm[bidx, p].clone()
-        perm[bidx, p] = perm[:, j].clone()
-        perm[:, j] = pp
-        rjj = norms[:, j].clamp(min=0).sqrt()
-        newly = (~done) & (rjj <= tol * r00)
-        ranks = torch.where(newly, torch.full_like(ranks, j), ranks)
-        done = done | newly
-        if (j & 15) == 15 and bool(done.all()):
-            break
-        x = At[:, j, j:]
-        x0 = x[:, 0]
-        ax0 = x0.abs()
-        if At.is_complex():
-            phase = torch.where(ax0 > 0, x0 / torch.where(ax0 > 0, ax0, 1.0), torch.ones_like(x0))
-        else:
-            phase = torch.where(x0 < 0, -1.0, 1.0).to(x0.dtype)
-        alpha = -phase * rjj
-        v = x.clone()
-        v[:, 0] -= alpha
-        vn = (v.abs() ** 2).sum(-1).sqrt()
-        v = v / torch.where(vn > 0, vn, 1.0).to(v.dtype)[:, None]
-        if j + 1 < C:
-            Tr = At[:, j + 1:, j:]
-            w = torch.bmm(Tr, v.conj().unsqueeze(-1))             # (B, C-j-1, 1)
-            Tr.sub_(2.0 * w * v.unsqueeze(1))
-            tail = At[:, j + 1:, j + 1:]
-            norms[:, j + 1:] = (tail.real ** 2 + (tail.imag ** 2 if tail.is_complex() else 0)).sum(-1)
-        At[:, j, j] = alpha
-        At[:, j, j + 1:] = 0
-    return ranks, perm
+    At: (B, C, R) contiguous.  Returns (ranks (B,), perm (B, C)); on return
+    At[b, c, r] = R_b[r, c] for r < ranks[b] (the first ranks[b] rows of the
+    upper-triangular factor of A_b[:, perm_b])."""
+    return devkern.cpqr(At, tol)  # (raises on a non-contiguous At: the caller reads R from it)
 
 
 # ------------------------------------------------------------------ builder
@@ -299,7 +225,7 @@ def _process_chunk(basis, rows_l, cols_l, chunk, tol, final, device, gen, budget
             # (Cmax - c)-th smallest onwards
             lam = ev[j, Cmax - c:]
             smin = float(lam[0].clamp(min=0).sqrt())
-            fro = math.sqrt(Rs[i] * c) if isinstance(basis, TorchFlatBasis) else None
+            fro = math.sqrt(Rs[i] * c) if isinstance(basis, DeviceFlatBasis) else None
             if fro is None:
                 fro = float(_fro_norm(basis, rows_l[chunk[i]], cols_l[chunk[i]], device))
             if smin > tol * fro * 4.0:

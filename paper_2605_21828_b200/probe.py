@@ -33,7 +33,7 @@ import numpy as np
 
 import mht_inputs as mi
 
-from .precompute.gpu_builder import OVERSAMPLE, TorchFlatBasis, cpqr_batched
+from .precompute.gpu_builder import OVERSAMPLE, DeviceFlatBasis, cpqr_batched
 from .precompute.trees import freq_tree, kd_tree
 
 
@@ -68,7 +68,7 @@ def probe(w: mi.Workload, samples: int = 16, seed: int = 0, device="cuda", log=p
     perm, sp_off = kd_tree(x, L, alternate=True)
     fr_off = freq_tree(m, L)
     log(f"[probe] trees in {time.time() - t0:.1f}s")
-    basis = TorchFlatBasis(x, k, device)
+    basis = DeviceFlatBasis(x, k, device)
     gen = torch.Generator(device=device)
     gen.manual_seed(1234 + seed)
     rng = np.random.default_rng(seed)

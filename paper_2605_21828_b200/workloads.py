@@ -67,20 +67,21 @@ def setup(w: mi.Workload):
 
 def build_workload_plan(w: mi.Workload, path: str, workers=None, log=print, precompute_sphere=None,
                         builder: str = "cpu", device="cuda"):
-    """builder = "cpu" (numpy/scipy CPQR, multiprocess) or "gpu" (batched
-    torch CPQR on the device; same factorization, same file format)."""
+    """builder = "cpu" (numpy/scipy CPQR, multiprocess) or "gpu" (libmht's
+    construction kernels on the device, include/mht_build.h; same
+    factorization, same file format)."""
     basis, perm, sp_off, fr_off, perm_k = setup(w)
     if builder == "gpu":
         from .precompute import gpu_builder as G
 
         if w.family == "flat":
-            tb = G.TorchFlatBasis(basis.x, basis.k, device)
+            tb = G.DeviceFlatBasis(basis.x, basis.k, device)
         elif w.family == "sphere":
-            tb = G.TorchTableBasis(G.sphere_table_torch(basis.theta, basis.phi, basis.lmax, device), np.float64)
+            tb = G.DeviceTableBasis(G.sphere_table(basis.theta, basis.phi, basis.lmax, device), np.float64)
         else:
             import torch
 
-            tb = G.TorchTableBasis(torch.as_tensor(np.asarray(basis.Phi), device=device), basis.dtype)
+            tb = G.DeviceTableBasis(torch.as_tensor(np.asarray(basis.Phi), device=device), basis.dtype)
         try:
             return G.build_plan_gpu(tb, perm, sp_off, fr_off, w.L, w.tol, path, device=device, log=log,
                                     perm_k=perm_k)
@@ -92,7 +93,7 @@ def build_workload_plan(w: mi.Workload, path: str, workers=None, log=print, prec
 
 
 # bump when the builders' numerics change so cached plans are never reused across versions
-BUILDER_VERSION = 5  # 5: quadtree-frequency plans carry perm_k (plan v2)
+BUILDER_VERSION = 6  # 5: quadtree-frequency plans carry perm_k (plan v2); 6: device CPQR kernel (per-block stop)
 
 
 def plan_cache_path(w: mi.Workload, root: str | None = None) -> str:

@@ -1,5 +1,6 @@
 """CPU-side checks of the boundary: libmht.so builds for sm_100a, loads, and
-exports every symbol include/mht.h declares (no compute calls without a GPU)."""
+exports every symbol include/mht.h and include/mht_build.h declare (no compute
+calls without a GPU)."""
 import ctypes
 import os
 import re
@@ -10,9 +11,9 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
-    src = open(os.path.join(ROOT, "include", "mht.h")).read()
-    return sorted(set(re.findall(r"\b(mht_[a-z_]+)\s*\(", src)))
+def declared_symbols(header="mht.h", prefix="mht_"):
+    src = open(os.path.join(ROOT, "include", header)).read()
+    return sorted(set(re.findall(rf"\b({prefix}[a-z_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
@@ -31,6 +32,29 @@ def test_library_exports_every_declared_symbol(libpath):
     out = subprocess.run(["nm", "-D", "--defined-only", libpath], capture_output=True, text=True).stdout
     for s in syms:
         assert re.search(rf"\bT {s}$", out, re.M), s
+
+
+def test_library_exports_build_kernels(libpath):
+    """include/mht_build.h (NEXT-1 plan-construction kernels)."""
+    syms = declared_symbols("mht_build.h", "mhtb_")
+    assert syms == ["mhtb_cpqr", "mhtb_flat_blocks", "mhtb_sphere_table"]
+    out = subprocess.run(["nm", "-D", "--defined-only", libpath], capture_output=True, text=True).stdout
+    for s in syms:
+        assert re.search(rf"\bT {s}$", out, re.M), s
+
+
+def test_build_kernels_reject_bad_args_without_gpu(libpath):
+    from paper_2605_21828_b200.precompute import devkern
+
+    L = devkern._lib()
+    assert L.mhtb_flat_blocks(None, None, None, None, -1, 1, 1, None, None) == 1
+    assert L.mhtb_flat_blocks(None, None, None, None, 1, 1, 1, None, None) == 1
+    assert L.mhtb_sphere_table(None, None, 4, -1, None, None) == 1
+    assert L.mhtb_cpqr(None, 1, 1, 1, 7, 1e-8, None, None, None) == 1
+    assert L.mhtb_cpqr(None, 1, 4, 4, 2, 1e-8, None, None, None) == 1
+    # nothing to do: no device touched
+    assert L.mhtb_flat_blocks(None, None, None, None, 0, 5, 5, None, None) == 0
+    assert L.mhtb_cpqr(None, 0, 4, 4, 1, 1e-8, None, None, None) == 0
 
 
 def test_binding_names_match_header():
