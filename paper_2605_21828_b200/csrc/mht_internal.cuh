@@ -143,13 +143,9 @@ void lsqr_update(bool cplx, void *v, void *w, void *x, int64_t len, int k, const
 void lsqr_xnorm(bool cplx, const void *x, int64_t len, int k, double *partial, LsqrCol *col, void *stream);
 
 // Launchers (mht_kernels.cu).  is_complex selects double2 vs double.
-// variant (picked per stage by the loader): FWD_STREAM (stages of many
-// waves), FWD_LATENCY (x staged per chunk, balanced batches, L2 prefetch),
-// FWD_PRE (factor sub-tile and gather addresses fetched before the
-// dependency wait; column chunks of at most fwd_pre_cols() columns).
-enum : int { FWD_STREAM = 0, FWD_LATENCY = 1, FWD_PRE = 2 };
-void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, int variant, void *stream);
-int fwd_pre_cols(bool is_complex);
+// latency: the few-tile variant (x staged per chunk, balanced batches, L2
+// prefetch) instead of the streaming one; the loader picks per stage.
+void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool latency, void *stream);
 void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f, void *stream);
 // multi-RHS (nrhs >= 2): DMMA kernels; forward uses the 64-row tiles, the
 // adjoint uses 64-column tiles (adjm lists).

@@ -1639,157 +1639,6 @@ __global__ void __launch_bounds__(256) reduce_kernel(const Ctx cx, const Piece *
 
 
 // ------------------------------------------------------------------------
-// nrhs = 1 forward, prefetch variant (stages of small plans and the small
-// stages of large ones).  One CTA per (block, 64-row tile, column chunk of at
-// most PRE_COLS columns).  Everything that depends only on the plan is
-// fetched BEFORE griddepcontrol.wait, so a CTA that becomes resident while the
-// previous stage still runs (its tail, or all of it when the stages are
-// small) has its work in shared memory when the dependency resolves:
-//   * the whole factor sub-tile, by 16-byte cp.async from all threads at once
-//     (one memory round trip, not a batch loop; 64 KB per CTA, 3 CTAs/SM);
-//   * the gather indices of its columns and of its skeleton rows (perm_k
-//     resolved too).
-// After the wait only the input values (x for the columns, z for the
-// skeleton rows) are loaded — one round trip — then the products come from
-// shared memory, and a split's partial rows are combined by the group's last
-// CTA (atomic arrival counter, sums in split order: deterministic).
-// ------------------------------------------------------------------------
-// PRE_KB: KB of factor sub-tile per CTA (64: 64 columns complex / 128 real, 3 CTAs per SM)
-template <class S, int KB>
-__host__ __device__ constexpr int pre_cols() { return KB * 1024 / (FWD_ROWS * (int)sizeof(S)); }
-template <int KB>
-constexpr int pre_minb() { return KB >= 64 ? 3 : (KB >= 32 ? 6 : 8); }
-
-// the plan-side half of in_value(): where in[q] lives (no user data touched)
-struct InRef {
-  int64_t off;  // element offset: user c index (SRC_C, perm_k applied) or zpool entry (SRC_Z)
-  int src;
-};
-__device__ __forceinline__ InRef in_ref(const Ctx &cx, const DevBlock &B, int q) {
-  const bool s1 = q >= B.seg_len[0];
-  const int64_t off = s1 ? B.seg_off[1] + (q - B.seg_len[0]) : B.seg_off[0] + q;
-  const int32_t src = s1 ? B.seg_src[1] : B.seg_src[0];
-  return InRef{src == SRC_C ? user_c_index(cx, off) : off, src};
-}
-// the data half (after griddepcontrol.wait): nrhs = 1
-template <class S>
-__device__ __forceinline__ S in_load(const Ctx &cx, InRef a) {
-  if (a.src == SRC_C) {
-    const S v = static_cast<const S *>(cx.c)[a.off];
-    return cx.diag ? Tr<S>::scale(v, diag_at(cx, a.off)) : v;
-  }
-  return static_cast<const S *>(cx.z)[a.off];
-}
-
-template <class S, int KB>
-__global__ void __launch_bounds__(FWD_THREADS, pre_minb<KB>()) fwd_pre_kernel(const Ctx cx, const Tile *__restrict__ tiles) {
-  using X = Tr<S>;
-  constexpr bool REAL = sizeof(S) == 8;
-  constexpr int TC = pre_cols<S, KB>();
-  extern __shared__ __align__(16) unsigned char pre_smem[];
-  S *Ts = reinterpret_cast<S *>(pre_smem);  // [TC][FWD_ROWS]: column j of the tile at Ts + j * 64
-  __shared__ S xs[TC];
-  __shared__ S sk[FWD_ROWS];
-  __shared__ S red[2][FWD_ROWS];
-  __shared__ int last;
-  pdl_trigger();
-  const Tile tl = tiles[blockIdx.y];
-  const DevBlock B = cx.blocks[tl.blk];
-  const int tid = threadIdx.x;
-  const bool split = tl.pad >= 0;
-  int jbeg = 0, jend = B.n_red;
-  if (split) {
-    const int chunk = ((B.n_red + B.pad - 1) / B.pad + 31) & ~31;  // <= TC (loader)
-    jbeg = (tl.pad & 255) * chunk;
-    jend = min(B.n_red, jbeg + chunk);
-  }
-  const int nc = jend - jbeg, cnt = tl.count;
-  // ---- plan-side prologue: the factor sub-tile and the gather addresses
-  {
-    const S *T = static_cast<const S *>(cx.coef) + B.coef_off + (int64_t)jbeg * B.ld + tl.start;
-    if constexpr (REAL) {
-      // 16 bytes = a row pair (columns 16-byte aligned, zero pad row: loader repack)
-      const int pairs = (cnt + 1) >> 1;
-      for (int e = tid; e < nc * 32; e += FWD_THREADS) {
-        const int j = e >> 5, pr = e & 31;
-        if (pr < pairs) cp_async<16>(Ts + j * FWD_ROWS + 2 * pr, T + (int64_t)j * B.ld + 2 * pr, true);
-      }
-    } else {
-      for (int e = tid; e < nc * FWD_ROWS; e += FWD_THREADS) {
-        const int j = e >> 6, i = e & 63;
-        if (i < cnt) cp_async<16>(Ts + j * FWD_ROWS + i, T + (int64_t)j * B.ld + i, true);
-      }
-    }
-    cp_async_commit();
-  }
-  // thread t < nc gathers x for column jbeg + t; thread 64 + i (TC <= 64) or
-  // i (TC = 128: second slot) the skeleton value of row i
-  InRef xr{0, -1}, sr{0, -1};
-  if (tid < nc) {
-    const int q = (B.flags & F_RED_IOTA) ? jbeg + tid : cx.idx[B.red_off + jbeg + tid];
-    xr = in_ref(cx, B, q);
-  }
-  constexpr bool SK_LOW = TC > 64;
-  const int srow = SK_LOW ? tid : tid - 64;
-  const bool has_skel = srow >= 0 && srow < cnt && tl.start + srow < B.n_skel;
-  if (has_skel) {
-    const int row = tl.start + srow;
-    const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
-    sr = in_ref(cx, B, q);
-  }
-  const int orow = tid < cnt && (B.flags & F_OUT_F) ? cx.perm[B.out_off + tl.start + tid] : 0;  // leaf scatter
-  pdl_wait();
-  // ---- the dependency is resolved: input values (one round trip)
-  if (xr.src >= 0) xs[tid] = in_load<S>(cx, xr);
-  if (SK_LOW ? tid < FWD_ROWS : tid >= 64) sk[srow] = has_skel ? in_load<S>(cx, sr) : X::zero();
-  cp_async_wait_all();
-  __syncthreads();
-  // ---- products from shared memory: thread (row, half), halves interleave columns
-  {
-    const int row = tid & 63, half = tid >> 6;
-    S acc = X::zero();
-    const S *tc = Ts + row;
-#pragma unroll 8
-    for (int j = half; j < nc; j += 2) X::fma(acc, tc[j * FWD_ROWS], xs[j]);
-    red[half][row] = acc;
-  }
-  __syncthreads();
-  S *scratch = static_cast<S *>(cx.fsplit);
-  const int grp = tl.pad >> 8;
-  if (split) {
-    if (tid < FWD_ROWS)
-      scratch[B.fsp_off + ((int64_t)(tl.start / FWD_ROWS) * B.pad + (tl.pad & 255)) * FWD_ROWS + tid] =
-          X::add(red[0][tid], red[1][tid]);
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) last = atomicAdd(cx.fcount + grp, 1) == B.pad - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-  }
-  if (tid < cnt) {
-    S s;
-    if (split) {
-      s = X::zero();
-      for (int k = 0; k < B.pad; ++k)
-        s = X::add(s, X::ldcg(scratch + B.fsp_off + ((int64_t)(tl.start / FWD_ROWS) * B.pad + k) * FWD_ROWS + tid));
-    } else {
-      s = X::add(red[0][tid], red[1][tid]);
-    }
-    const int row = tl.start + tid;
-    if (row < B.n_skel) s = X::add(s, sk[tid]);
-    if (B.flags & F_OUT_F)
-      static_cast<S *>(cx.fout)[orow] = s;
-    else
-      static_cast<S *>(cx.z)[B.out_off + row] = s;
-  }
-  if (split && tid == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
-}
-
-template <class S, int KB>
-constexpr int pre_smem_bytes() { return pre_cols<S, KB>() * FWD_ROWS * (int)sizeof(S); }
-
-// ------------------------------------------------------------------------
 // Dataflow nrhs = 1 apply ("flow" kernels): ONE launch walks every phase of a
 // direction (forward: stages 0..L+1; adjoint: the leaf stage, then per stage
 // the unfused group sums and the stage, then the sums into c) with no grid
@@ -1924,14 +1773,10 @@ __global__ void __launch_bounds__(FL_THREADS, FL_MINB) flow_kernel(const Ctx cx,
 constexpr int MAX_GRID_Y = 65535;
 
 template <class S>
-void fwd_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int variant, cudaStream_t st) {
-  if (variant == FWD_PRE) smem_optin<fwd_pre_kernel<S, 64>>(pre_smem_bytes<S, 64>());
+void fwd_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, bool latency, cudaStream_t st) {
   for (int t0 = 0; t0 < ntiles; t0 += MAX_GRID_Y) {
     const int nt = ntiles - t0 < MAX_GRID_Y ? ntiles - t0 : MAX_GRID_Y;
-    if (variant == FWD_PRE)
-      launch_ex(PDL_NRHS1, fwd_pre_kernel<S, 64>, dim3(1, nt), dim3(FWD_THREADS), pre_smem_bytes<S, 64>(), st, cx,
-                tiles + t0);
-    else if (variant == FWD_LATENCY)
+    if (latency)
       launch_pdl(fwd_lat_kernel<S>, dim3(1, nt), dim3(FWD_THREADS), st, cx, tiles + t0);
     else
       launch_pdl(fwd_kernel<S>, dim3(1, nt), dim3(FWD_THREADS), st, cx, tiles + t0);
@@ -1948,15 +1793,13 @@ void adj_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cuda
 
 }  // namespace
 
-void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, int variant, void *stream) {
+void launch_fwd(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool latency, void *stream) {
   if (ntiles <= 0) return;
   if (is_complex)
-    fwd_dispatch<double2>(ctx, tiles, ntiles, variant, (cudaStream_t)stream);
+    fwd_dispatch<double2>(ctx, tiles, ntiles, latency, (cudaStream_t)stream);
   else
-    fwd_dispatch<double>(ctx, tiles, ntiles, variant, (cudaStream_t)stream);
+    fwd_dispatch<double>(ctx, tiles, ntiles, latency, (cudaStream_t)stream);
 }
-
-int fwd_pre_cols(bool is_complex) { return is_complex ? pre_cols<double2, 64>() : pre_cols<double, 64>(); }
 
 void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f, void *stream) {
   if (ntiles <= 0) return;

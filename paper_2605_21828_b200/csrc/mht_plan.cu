@@ -121,10 +121,9 @@ struct mht_plan {
   int64_t *d_rd = nullptr;
 
   std::vector<Range> fwd, fwd1, adj, adjm, pieces;  // per stage 0..L+1
-  // nrhs = 1 forward variant per stage (FWD_STREAM / FWD_LATENCY / FWD_PRE,
-  // mht_internal.cuh): prefetch for stages of <= 512 MB of factors, else
-  // latency for fewer than two waves of tiles at 7 CTAs per SM, else streaming
-  std::vector<int> fwd1_var;
+  // nrhs = 1 forward variant per stage: 1 = latency (fewer than two waves of
+  // tiles at 7 CTAs per SM), 0 = streaming
+  std::vector<char> fwd1_lat;
   std::vector<Range> pieces_u;  // pieces of the producers that are not fused (fused mode)
   // sharded plans (mht_plan_load_shard): G ranks, this is rank g, switch level ls;
   // exchange layout in zpool entries (x nrhs scalars each)
@@ -857,33 +856,13 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
   P->fwd1.assign(L + 2, Range{});
   int64_t split_scalars = 0;
   int32_t groups = 0;
-  // Stages of at most PRE_MAX_BYTES of factors run the prefetch variant
-  // (FWD_PRE): every tile's column chunk holds at most fwd_pre_cols() columns
-  // so its factor sub-tile fits one CTA's shared memory.
-  const int64_t PRE_MAX_BYTES = 512ll << 20;
-  const int pre_var = FWD_PRE;
-  const int pre_tc = fwd_pre_cols(P->cplx);
-  P->fwd1_var.assign(L + 2, FWD_STREAM);
-  for (int s = 0; s < L + 2; ++s) {
-    int64_t bytes = 0;
-    bool fits = true;
-    for (auto &x : ft[s]) {
-      const DevBlock &D = blocks[x.second.blk];
-      bytes += (int64_t)x.second.count * D.n_red * (int64_t)P->ssz;
-      fits = fits && D.n_red <= 255 * pre_tc;
-    }
-    if (!ft[s].empty() && fits && bytes <= PRE_MAX_BYTES) P->fwd1_var[s] = pre_var;
-  }
   for (int s = 0; s < L + 2; ++s) {
     const int nt = (int)ft[s].size();
-    const bool pre = P->fwd1_var[s] == pre_var;
     std::vector<std::pair<int64_t, Tile>> lst;
     for (auto &x : ft[s]) {
       DevBlock &D = blocks[x.second.blk];
       int ks = 1;
-      if (pre) {
-        ks = (D.n_red + pre_tc - 1) / pre_tc;
-      } else if (nt > 0 && nt < FWD1_TARGET && D.n_red >= 2 * FWD1_MIN_SPLIT) {
+      if (nt > 0 && nt < FWD1_TARGET && D.n_red >= 2 * FWD1_MIN_SPLIT) {
         ks = (FWD1_TARGET + nt - 1) / nt;
         ks = std::min(ks, D.n_red / FWD1_MIN_SPLIT);
         ks = std::min(ks, 255);
@@ -915,8 +894,8 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
     P->fwd1[s] = Range{(int32_t)fwd1_all.size(), (int32_t)lst.size()};
     for (auto &x : lst) fwd1_all.push_back(x.second);
   }
-  for (int s = 0; s < L + 2; ++s)
-    if (P->fwd1_var[s] != pre_var && P->fwd1[s].count < 2 * 7 * prop.multiProcessorCount) P->fwd1_var[s] = FWD_LATENCY;
+  P->fwd1_lat.assign(L + 2, 0);
+  for (int s = 0; s < L + 2; ++s) P->fwd1_lat[s] = P->fwd1[s].count < 2 * 7 * prop.multiProcessorCount ? 1 : 0;
   P->n_split_groups = groups;
   P->m_slabs = mslabs;
   P->m_groups = mgroups;
@@ -1265,7 +1244,7 @@ mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs, int part =
   for (int s = s_lo; s <= s_hi; ++s)
     timed(P, 0, s, nrhs, nrhs == 1 ? P->fwd1[s].count : P->fwd[s].count, [&] {
       if (nrhs == 1)
-        launch_fwd(P->cplx, cx, P->d_fwd1 + P->fwd1[s].off, P->fwd1[s].count, P->fwd1_var[s], P->stream);
+        launch_fwd(P->cplx, cx, P->d_fwd1 + P->fwd1[s].off, P->fwd1[s].count, P->fwd1_lat[s] != 0, P->stream);
       else
         launch_mma(P->cplx, false, cx, P->d_fwd + P->fwd[s].off, P->fwd[s].count, false, P->stream);
     });
