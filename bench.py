@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -79,10 +80,14 @@ class ClockSampler:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.p = None
 
-    def start(self):
+    def start(self, settle: float = 0.3):
+        """Start sampling; then wait `settle` s so nvidia-smi's start-up (NVML
+        initialisation, which can stall the driver for milliseconds) is over
+        before the caller's timed region begins."""
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                                        "-lms", "200", "-i", str(self.idx)], stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(settle)
         except Exception:
             self.p = None
 
@@ -533,10 +538,11 @@ def run_shard(args, w, path, ws, rank, lrank):
 
 
 def _e2e(P, phases, w, ws, args, device_ms_per_step=None):
-    """The same step through the C ABI's host-buffer calls (mht_apply_host /
-    mht_apply_adjoint_host): every phase copies its input from pinned host
-    memory, replays the apply and copies the result back, inside the timed
-    region.  Also measures the host<->device link on this box (pinned torch
+    """The same step through the C ABI's host-buffer call mht_apply_host_batch:
+    every phase copies its input from pinned host memory, replays the apply
+    and copies the result back, inside the timed region, the copies of one
+    phase overlapping the transforms of its neighbours (one call per step,
+    which returns when all of the step's outputs are in host memory).  Also measures the host<->device link on this box (pinned torch
     copies of the widest phase's vectors, CUDA events, each direction alone)
     so the e2e time can be checked against device time + bytes / link rate."""
     import torch
@@ -552,24 +558,31 @@ def _e2e(P, phases, w, ws, args, device_ms_per_step=None):
         h2d += ti.numel() * P.scalar_bytes
         d2h += to.numel() * P.scalar_bytes
 
+    # one pipelined host batch per step (mht_apply_host_batch): each phase's
+    # input copy and the previous phase's output copy overlap the transforms;
+    # the call returns when the step's outputs are all in host memory
+    jobs = [(0 if kind == "fwd" else 1, r, host_in[(kind, r)].data_ptr(), host_out[(kind, r)].data_ptr())
+            for kind, r in phases]
+
     def step():
-        for kind, r in phases:
-            ti, to = host_in[(kind, r)], host_out[(kind, r)]
-            if kind == "fwd":
-                P.apply_host_ptr(ti.data_ptr(), to.data_ptr(), r)
-            else:
-                P.adjoint_host_ptr(ti.data_ptr(), to.data_ptr(), r)
+        P.host_batch_ptr(jobs)
 
     # two warm-up steps: the first grows the host staging to the widest phase
     # (which drops the graphs captured for the narrower ones), the second
     # captures every phase's graph outside the timed region
     step()
     step()
+    # at least args.e2e_steps steps and ~0.2 s of them (small plans: 1 ms steps),
+    # the same count on every rank
+    nsteps = args.e2e_steps
+    if device_ms_per_step:
+        nsteps = max(nsteps, int(math.ceil(200.0 / max(device_ms_per_step, 1e-3))))
+    nsteps = int(allreduce_max(nsteps, ws))
     barrier(ws)
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
     t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
+    for _ in range(nsteps):
         step()
     el = allreduce_max(time.perf_counter() - t0, ws)
     clk = clocks.stop()
@@ -591,12 +604,13 @@ def _e2e(P, phases, w, ws, args, device_ms_per_step=None):
             t = a.elapsed_time(b)
             best = t if best is None else min(best, t)
         rates[name] = src_.numel() * P.scalar_bytes / (best / 1e3) / 1e9
-    out = {"value": ws * transforms * args.e2e_steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "ms_per_step": 1e3 * el / args.e2e_steps,
+    out = {"value": ws * transforms * nsteps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "steps": nsteps, "ms_per_step": 1e3 * el / nsteps,
            "link_GBps": {"h2d": rates["h2d"], "d2h": rates["d2h"],
                          "how": "pinned torch copy of the widest phase's vector, best of 5, CUDA events"},
            "clocks": clk,
-           "api": "mht_apply_host / mht_apply_adjoint_host (pinned host buffers, copies in the timed region)"}
+           "api": "mht_apply_host_batch: the step's phases as one pipelined host batch (pinned host buffers, every "
+                  "copy in the timed region, host-to-device / device-to-host overlapping the transforms)"}
     if device_ms_per_step is not None:
         out["copy_floor_ms_per_step"] = 1e3 * (h2d / (rates["h2d"] * 1e9) + d2h / (rates["d2h"] * 1e9))
         out["device_ms_per_step"] = device_ms_per_step

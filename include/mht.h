@@ -131,6 +131,25 @@ mht_status mht_apply_adjoint(mht_plan *plan, const void *f, void *c, int nrhs);
 mht_status mht_apply_host(mht_plan *plan, const void *c_host, void *f_host, int nrhs);
 mht_status mht_apply_adjoint_host(mht_plan *plan, const void *f_host, void *c_host, int nrhs);
 
+/* A batch of independent host-buffer transforms, pipelined (the serving
+ * loop's end-to-end path): job i is a synthesis (dir 0: in = c, m x nrhs;
+ * out = f, n x nrhs) or an analysis (dir 1: in = f, out = c;
+ * P:153-155), both host pointers in the ABI layout (pinned for full copy
+ * bandwidth).  Job i's host-to-device copy and job i-1's device-to-host copy
+ * run on the plan's copy streams while job i-1 / job i transform, through two
+ * device staging slots ordered by events, so copies overlap the transforms.
+ * Returns when every output is in host memory.  Results are bitwise those of
+ * mht_apply_host / mht_apply_adjoint_host.  Inputs and outputs must not
+ * overlap each other.  Errors: MHT_ERR_INVALID_ARG (null plan or job pointer,
+ * dir not 0/1, nrhs < 1, sharded plan), MHT_ERR_OOM, MHT_ERR_CUDA. */
+typedef struct {
+  int32_t dir;  /* 0 synthesis, 1 analysis */
+  int32_t nrhs;
+  const void *in;
+  void *out;
+} mht_host_job;
+mht_status mht_apply_host_batch(mht_plan *plan, const mht_host_job *jobs, int njobs);
+
 /* ---- sharded plans: one plan across G GPUs -----------
  * The factorization is split at a switch level ls (log2 G <= ls <= L - log2 G;
  * switch_level < 0 picks max(log2 G, L/2)).  Rank g holds, for stages 0..ls,

@@ -160,6 +160,13 @@ struct mht_plan {
   int ws_nrhs = 0;
   void *d_hc = nullptr, *d_hf = nullptr;
   int host_nrhs = 0;
+  // mht_apply_host_batch: copy streams (in / out), two device staging slots
+  // (input and output buffers of max(m, n) x nrhs scalars each) and per-slot
+  // events: input landed, transform done, output read back
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  void *d_bin[2] = {nullptr, nullptr}, *d_bout[2] = {nullptr, nullptr};
+  int64_t bcap = 0;  // scalars per staging buffer
+  cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
   // mht_lsqr work vectors (u, v, w, Phi v, Phi^* u, norm partials, per-column
   // state), kept across calls and grown with nrhs so repeated solves reuse the
   // same pointers (and the captured graphs keyed on them)
@@ -181,6 +188,17 @@ struct mht_plan {
     clear_graphs();
     if (own_stream && own_stream != stream) cudaStreamSynchronize(own_stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    for (cudaStream_t q : {s_in, s_out})
+      if (q) {
+        cudaStreamSynchronize(q);
+        cudaStreamDestroy(q);
+      }
+    for (int i = 0; i < 2; ++i) {
+      for (cudaEvent_t e : {ev_in[i], ev_comp[i], ev_out[i]})
+        if (e) cudaEventDestroy(e);
+      for (void *p : {d_bin[i], d_bout[i]})
+        if (p) cudaFree(p);
+    }
     if (own_stream) cudaStreamDestroy(own_stream);
     for (void *p : lsqr_buf)
       if (p) cudaFree(p);
@@ -1706,6 +1724,75 @@ mht_status mht_apply_adjoint_host(mht_plan *P, const void *f_host, void *c_host,
   if ((s = run_dir(P, 1, P->d_hf, P->d_hc, nrhs)) != MHT_OK) return s;
   CUDA_TRY(cudaMemcpyAsync(c_host, P->d_hc, (size_t)P->m * nrhs * P->ssz, cudaMemcpyDeviceToHost, P->stream));
   CUDA_TRY(cudaStreamSynchronize(P->stream));
+  return MHT_OK;
+}
+
+// Batch of independent host-buffer transforms, pipelined: job i's input copy
+// (stream s_in) overlaps job i-1's transform (the plan's stream) and job i-2's
+// output copy (stream s_out); two staging slots, ordered by events.
+mht_status mht_apply_host_batch(mht_plan *P, const mht_host_job *jobs, int njobs) {
+  if (!P || (njobs > 0 && !jobs) || njobs < 0) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G > 1) return fail(MHT_ERR_INVALID_ARG, "sharded plan: use the mht_*_shard_* calls");
+  int maxr = 0;
+  for (int i = 0; i < njobs; ++i) {
+    const mht_host_job &J = jobs[i];
+    if ((J.dir != 0 && J.dir != 1) || J.nrhs < 1 || !J.in || !J.out) return fail(MHT_ERR_INVALID_ARG, "bad job");
+    maxr = std::max(maxr, J.nrhs);
+  }
+  if (njobs == 0) return MHT_OK;
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status st;
+  if ((st = ensure_ws(P, maxr)) != MHT_OK) return st;
+  const int64_t need = std::max(P->m, P->n) * (int64_t)maxr;
+  if (!P->s_in) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->s_in, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->s_out, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t *e : {&P->ev_in[i], &P->ev_comp[i], &P->ev_out[i]})
+        CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  if (need > P->bcap) {
+    CUDA_TRY(cudaStreamSynchronize(P->s_out));
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    P->clear_graphs();
+    for (int i = 0; i < 2; ++i) {
+      for (void *q : {P->d_bin[i], P->d_bout[i]})
+        if (q) cudaFree(q);
+      P->d_bin[i] = P->d_bout[i] = nullptr;
+    }
+    P->bcap = 0;
+    for (int i = 0; i < 2; ++i) {
+      CUDA_TRY(cudaMalloc(&P->d_bin[i], (size_t)need * P->ssz));
+      CUDA_TRY(cudaMalloc(&P->d_bout[i], (size_t)need * P->ssz));
+    }
+    P->bcap = need;
+  }
+  // the slots may still be in use by a previous batch's tail: start after it
+  CUDA_TRY(cudaEventRecord(P->ev_out[0], P->s_out));
+  CUDA_TRY(cudaEventRecord(P->ev_out[1], P->s_out));
+  CUDA_TRY(cudaEventRecord(P->ev_comp[0], P->stream));
+  CUDA_TRY(cudaEventRecord(P->ev_comp[1], P->stream));
+  for (int i = 0; i < njobs; ++i) {
+    const mht_host_job &J = jobs[i];
+    const int sl = i & 1;
+    const size_t in_b = (size_t)(J.dir == 0 ? P->m : P->n) * J.nrhs * P->ssz;
+    const size_t out_b = (size_t)(J.dir == 0 ? P->n : P->m) * J.nrhs * P->ssz;
+    // input: the slot's input buffer is free once job i-2's transform is done
+    CUDA_TRY(cudaStreamWaitEvent(P->s_in, P->ev_comp[sl], 0));
+    CUDA_TRY(cudaMemcpyAsync(P->d_bin[sl], J.in, in_b, cudaMemcpyHostToDevice, P->s_in));
+    CUDA_TRY(cudaEventRecord(P->ev_in[sl], P->s_in));
+    // transform: input landed and the slot's output buffer read back (job i-2)
+    CUDA_TRY(cudaStreamWaitEvent(P->stream, P->ev_in[sl], 0));
+    CUDA_TRY(cudaStreamWaitEvent(P->stream, P->ev_out[sl], 0));
+    if ((st = run_dir(P, J.dir, P->d_bin[sl], P->d_bout[sl], J.nrhs)) != MHT_OK) return st;
+    CUDA_TRY(cudaEventRecord(P->ev_comp[sl], P->stream));
+    // output
+    CUDA_TRY(cudaStreamWaitEvent(P->s_out, P->ev_comp[sl], 0));
+    CUDA_TRY(cudaMemcpyAsync(J.out, P->d_bout[sl], out_b, cudaMemcpyDeviceToHost, P->s_out));
+    CUDA_TRY(cudaEventRecord(P->ev_out[sl], P->s_out));
+  }
+  CUDA_TRY(cudaStreamSynchronize(P->s_out));
+  CUDA_TRY(cudaGetLastError());
   return MHT_OK;
 }
 

@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(HERE, "libmht.so")
 MHT_DTYPE_F64, MHT_DTYPE_C128 = 1, 2
 EXPORTED = [
     "mht_plan_load", "mht_plan_info_get", "mht_plan_set_stream", "mht_reserve", "mht_apply",
-    "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host", "mht_apply_diag", "mht_apply_adjoint_diag", "mht_grf_sample", "mht_covariance_apply", "mht_lsqr",
+    "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host", "mht_apply_host_batch", "mht_apply_diag", "mht_apply_adjoint_diag", "mht_grf_sample", "mht_covariance_apply", "mht_lsqr",
     "mht_plan_load_shard", "mht_shard_info", "mht_shard_workspace", "mht_apply_shard_begin",
     "mht_apply_shard_end", "mht_apply_adjoint_shard_begin", "mht_apply_adjoint_shard_end",
     "mht_set_graphs", "mht_set_fused_sums", "mht_set_persistent", "mht_phase_times", "mht_sync",
@@ -33,6 +33,11 @@ EXPORTED = [
 
 class MhtError(RuntimeError):
     pass
+
+
+class HostJob(C.Structure):
+    """mht_host_job (include/mht.h)."""
+    _fields_ = [("dir", C.c_int32), ("nrhs", C.c_int32), ("inp", C.c_void_p), ("out", C.c_void_p)]
 
 
 class PlanInfo(C.Structure):
@@ -63,6 +68,7 @@ def load_library(path: str = LIB_PATH):
         getattr(L, nm).argtypes = [vp, vp, vp, i32]
     for nm in ("mht_apply_diag", "mht_apply_adjoint_diag", "mht_grf_sample", "mht_covariance_apply"):
         getattr(L, nm).argtypes = [vp, vp, vp, vp, i32]
+    L.mht_apply_host_batch.argtypes = [vp, vp, i32]
     L.mht_lsqr.argtypes = [vp, vp, vp, i32, i32, C.c_double, C.c_double, C.POINTER(C.c_int32),
                            C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.mht_plan_load_shard.argtypes = [C.c_char_p, i32, i32, i32, i32, C.POINTER(vp)]
@@ -275,6 +281,27 @@ class Plan:
                                                      C.c_void_p(c_host.ctypes.data), nrhs),
                "mht_apply_adjoint_host")
         return c_host
+
+    def host_batch_ptr(self, jobs):
+        """mht_apply_host_batch over [(dir, nrhs, in_ptr, out_ptr), ...] (host
+        pointers in the ABI layout; the caller keeps the buffers alive)."""
+        arr = (HostJob * len(jobs))(*[HostJob(int(d), int(r), C.c_void_p(i), C.c_void_p(o)) for d, r, i, o in jobs])
+        self._stream()
+        _check(load_library().mht_apply_host_batch(self._h, arr, len(jobs)), "mht_apply_host_batch")
+
+    def host_batch(self, jobs):
+        """jobs: [(dir, host input array)] -> list of host outputs (numpy,
+        pinned-or-not; checked like apply_host)."""
+        ins, outs, spec = [], [], []
+        for d, x in jobs:
+            rows_in, rows_out = (self.m, self.n) if d == 0 else (self.n, self.m)
+            x = np.ascontiguousarray(x, dtype=self.np_dtype).reshape(-1, rows_in)
+            o = self._host_out(None, x.shape[0], rows_out)
+            ins.append(x)
+            outs.append(o)
+            spec.append((d, x.shape[0], x.ctypes.data, o.ctypes.data))
+        self.host_batch_ptr(spec)
+        return outs
 
     def apply_host_ptr(self, c_ptr: int, f_ptr: int, nrhs: int):
         self._stream()

@@ -243,6 +243,38 @@ def test_determinism_and_host_api(gpu, oracle_lib, plans):
     assert P.apply_host(c, out) is out and np.array_equal(out, fh)
 
 
+def test_host_batch_pipelined(gpu, oracle_lib, plans):
+    """mht_apply_host_batch (copies on the plan's copy streams overlapping the
+    transforms, two staging slots): mixed synthesis / analysis jobs at several
+    widths, more jobs than slots, pinned and pageable buffers, complex and real
+    plans — bitwise equal to the device-buffer applies and to O2 element by
+    element; two batches back to back; bad jobs rejected."""
+    path_c, wc = flat_case(plans, 2048, 32, 4, 1e-8)
+    sp = str(plans / "sph_batch.plan")
+    ws = W.sphere_workload(2048, 31, 4, 1e-10)
+    W.build_workload_plan(ws, sp, workers=8, log=None)
+    for path, w in ((path_c, wc), (sp, ws)):
+        P = gpu.Plan(path)
+        O = oracle_lib.Plan(path)
+        gen = mi.complex_gaussian if w.dtype == "complex128" else mi.real_gaussian
+        jobs = [(0, gen(1, w.m, 601)), (1, gen(1, w.n, 602)), (0, gen(32, w.m, 603)), (1, gen(3, w.n, 604)),
+                (0, gen(5, w.m, 605)), (1, gen(32, w.n, 606)), (0, gen(1, w.m, 607))]
+        for rep in range(2):
+            pinned = rep == 1
+            jj = [(d, torch.from_numpy(x).pin_memory().numpy() if pinned else x) for d, x in jobs]
+            outs = P.host_batch(jj)
+            for (d, x), o in zip(jobs, outs):
+                xt = torch.from_numpy(x).cuda()
+                ref = (P.apply(xt) if d == 0 else P.adjoint(xt)).cpu().numpy()
+                assert np.array_equal(o, ref), (path, d, x.shape, rep)
+                assert o2_err(o, O.apply(x) if d == 0 else O.adjoint(x)) <= PARITY
+        with pytest.raises(gpu.MhtError):
+            P.host_batch_ptr([(2, 1, 1, 1)])
+        with pytest.raises(gpu.MhtError):
+            P.host_batch_ptr([(0, 0, 1, 1)])
+        P.close()
+
+
 def test_adjoint_identity_gpu(gpu, oracle_lib, plans):
     path, w = flat_case(plans, 2048, 32, 4, 1e-8)
     P = gpu.Plan(path)
