@@ -18,9 +18,14 @@ timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gp
     --log-file gpurun_out/${tag}_c2_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e \
     > gpurun_out/${tag}_ncu_launches.log 2>&1
 echo "launch list rc=$?"
-for w in c2 c3; do
+for w in c2 c3 c1 c4 c2kd; do
   timeout 600 python tools/prof_run.py $w > gpurun_out/${tag}_prof_$w.log 2>&1 && \
   timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file gpurun_out/${tag}_${w}_traffic.csv python tools/prof_run.py $w > gpurun_out/${tag}_ncu_traffic_$w.log 2>&1
   echo "traffic $w rc=$?"
 done
+# the c5 stand-in (103.6 GB plan, built by the device builder) last: the longest
+if [ "${WITH_C5S:-0}" = "1" ]; then
+  timeout 3000 python bench.py --workload c5s --steps 5 --warmup 3 > gpurun_out/${tag}_bench_c5s.json 2> gpurun_out/${tag}_bench_c5s.err
+  echo "bench c5s rc=$?"; tail -c 300 gpurun_out/${tag}_bench_c5s.json; echo
+fi
