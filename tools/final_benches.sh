@@ -26,6 +26,7 @@ for w in c2 c3 c1 c4 c2kd; do
 done
 # the c5 stand-in (103.6 GB plan, built by the device builder) last: the longest
 if [ "${WITH_C5S:-0}" = "1" ]; then
+  rm -f /dev/shm/mht_plans/*.plan 2>/dev/null  # host RAM: the 104 GB plan file lives in /dev/shm
   timeout 3000 python bench.py --workload c5s --steps 5 --warmup 3 > gpurun_out/${tag}_bench_c5s.json 2> gpurun_out/${tag}_bench_c5s.err
   echo "bench c5s rc=$?"; tail -c 300 gpurun_out/${tag}_bench_c5s.json; echo
 fi

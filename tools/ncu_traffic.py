@@ -80,4 +80,11 @@ def main(src: str, workload: str, dst: str, width: int = 32):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]) if len(sys.argv) > 4 else 32)
+    if len(sys.argv) > 4:
+        wd = int(sys.argv[4])
+    else:  # the workload's multi-RHS width (tools/prof_run.py runs nrhs = 1 and that width)
+        import os
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import mht_inputs as mi
+        wd = max([r for r in mi.WORKLOADS[sys.argv[2]].nrhs if r > 1] or [32])
+    main(sys.argv[1], sys.argv[2], sys.argv[3], wd)
