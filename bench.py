@@ -59,6 +59,10 @@ def parse():
                     help="replicas (default): every rank holds the whole plan and transforms its own columns "
                          "(weak scaling, no data-path collective); shard: the plan is split across the ranks "
                          "and every transform is done jointly with one NCCL all-to-all (strong scaling)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
+                    help="--mode shard only: nccl = one all_to_all_single of z_ls per direction between the "
+                         "kernel sequences; fused = the switch stage's kernels store z_ls straight into the peers' "
+                         "receive buffers over NVLink peer memory (CUDA IPC) with arrival flags (DESIGN.md §7)")
     ap.add_argument("--cpu-table", action="store_true",
                     help="cpu_baseline leg only: time the oracle (O2 at 1 and all threads, O1 dense sum full or on "
                          "a labelled row subset) on this host for --workload, print one JSON line, exit")
@@ -486,6 +490,8 @@ def run_shard(args, w, path, ws, rank, lrank):
     dev = torch.device("cuda", lrank)
     S = SH.ShardPlan(path, ws, rank, lrank)
     phases = phases_for(w)
+    if args.exchange == "fused":
+        S.fuse(max(r for _, r in phases))
     ins, outs = {}, {}
     for kind, r in phases:
         if kind == "fwd":
@@ -526,6 +532,8 @@ def run_shard(args, w, path, ws, rank, lrank):
            "data": "synthetic (seeded generators in mht_inputs; no paper dataset)",
            "config": {"workload": workload_desc(w), "phases": [f"{k}@nrhs{r}" for k, r in phases],
                       "transforms_per_step": transforms, "parallelism": f"shard{ws} (switch level {S.ls})",
+                      "exchange": ("fused: switch-stage stores into the peers' receive buffers (CUDA IPC, NVLink)"
+                                   if args.exchange == "fused" else "NCCL all_to_all_single"),
                       "factor_entries_this_rank": S.info.factor_entries,
                       "exchange_bytes_per_rhs_per_direction_this_rank": exch * S.scalar_bytes},
            "clocks": clk, "gpu_launches": None}

@@ -188,6 +188,35 @@ mht_status mht_apply_shard_end(mht_plan *plan, void *f, int nrhs);
 mht_status mht_apply_adjoint_shard_begin(mht_plan *plan, const void *f, int nrhs);
 mht_status mht_apply_adjoint_shard_end(mht_plan *plan, void *c, int nrhs);
 
+/* Fused exchange (one process per GPU on one node, NVLink /
+ * NVSwitch peer memory): instead of an all-to-all between _begin and _end,
+ * the switch stage's kernels store every z_ls block bound for rank h straight
+ * into rank h's receive buffer (remote stores, so the transfer overlaps the
+ * stage's math tile by tile), and in the analysis the sums of z_ls's adjoint
+ * formed for rank g are stored straight into rank g's send buffer; _begin then
+ * signals every rank (system-scope release of a per-rank arrival flag after a
+ * system fence) and _end waits for every rank's flag before reading.  No
+ * collective library call is left on the data path.  All ranks must run the
+ * same sequence of sharded applies at the same nrhs (<= the set-up nrhs).
+ *   mht_shard_export:  sizes the workspace for `nrhs` right-hand sides and
+ *     writes this rank's IPC handle of it (cudaIpcMemHandle_t, 64 bytes; NULL
+ *     to skip) and its layout: layout[0..G) = receive offsets per source,
+ *     layout[G..2G) = send offsets per destination (workspace entries),
+ *     layout[2G] = the byte offset of its sync area (2 G + 2 u64, zeroed).
+ *   mht_shard_open_peers:  opens the other ranks' handles (ipc_handles: G x 64
+ *     bytes in rank order; this rank's entry is ignored) and sets them up.
+ *   mht_shard_set_peers:  the same from device pointers already mapped in this
+ *     process (bases[h] = rank h's workspace; bases[shard] must be this plan's
+ *     own) — the one-process emulation of G ranks on one GPU.
+ *   layouts: G x (2 G + 1) int64, rank h's export at h (2 G + 1).
+ *   mht_shard_close_peers: back to the all-to-all path, IPC mappings released.
+ * Errors: MHT_ERR_INVALID_ARG (not sharded, bad pointers, nrhs above the
+ * set-up width), MHT_ERR_OOM, MHT_ERR_CUDA (IPC failures included). */
+mht_status mht_shard_export(mht_plan *plan, int nrhs, void *ipc_handle, int64_t *layout);
+mht_status mht_shard_open_peers(mht_plan *plan, int nrhs, const void *ipc_handles, const int64_t *layouts);
+mht_status mht_shard_set_peers(mht_plan *plan, int nrhs, void *const *bases, const int64_t *layouts);
+mht_status mht_shard_close_peers(mht_plan *plan);
+
 /* ---- applications on top of the transform (§7) ----------------
  * A real diagonal on the coefficient side is fused into the transform's own
  * loads of c (synthesis) or its final stores of c (analysis): no extra pass

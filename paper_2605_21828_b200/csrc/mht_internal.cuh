@@ -19,6 +19,8 @@ enum : int32_t {
   F_SKEL_IOTA = 1,  // skeleton positions are 0..n_skel-1 (COPY blocks)
   F_RED_IOTA = 2,   // redundant positions are 0..n_red-1 (DENSE blocks)
   F_OUT_F = 4,      // output rows go to f through perm_x (leaf stage)
+  F_REMOTE = 8,     // sharded switch stage: outputs bound for rank (flags >> 16); with the
+                    // fused exchange on they are stored straight into that rank's receive buffer
 };
 
 // One materialised block: out[i] = in[skel[i]] (i < n_skel) + sum_j T[i,j] in[red[j]]
@@ -70,7 +72,7 @@ struct Piece {
   int32_t dst_src;  // SRC_C | SRC_Z
   int32_t len;
   int32_t rd_count;
-  int32_t pad;
+  int32_t remote;   // sharded: 1 + the rank whose send buffer this receive-buffer sum belongs to, else 0
 };
 
 struct Ctx {  // per-launch pointers
@@ -97,6 +99,13 @@ struct Ctx {  // per-launch pointers
   int fused;             // 1: adjoint inputs are summed from the partials on load
   int64_t m, n, Zt, Pt;  // Zt/Pt: workspace entries per RHS (layout [entry][rhs])
   int nrhs;
+  // fused exchange of a sharded plan (nullptr: off): zrem[h] / zdel[h] (h < G)
+  // the base and entry delta of rank h's receive buffer for this rank's
+  // switch-stage outputs, zrem[G + g] / zdel[G + g] those of rank g's send
+  // buffer for the adjoint sums formed here
+  void *const *zrem;
+  const int64_t *zdel;
+  int zG;
 };
 
 constexpr int FWD_ROWS = 64;     // rows per forward tile (2 per lane)
@@ -160,5 +169,12 @@ int persist_grid(bool is_complex);
 void launch_repack(const double *src, double *dst, const Repack *jobs, int njobs, void *stream);
 void launch_reduce(bool is_complex, const Ctx &ctx, const Piece *pieces, const int64_t *rd,
                    int npieces, void *stream);
+// fused exchange signalling (sharded plans): own_sync = this rank's
+// [2][G] arrival flags then its 2 epoch counters; peer_sync[h] = rank h's.
+// signal: epoch[dir] += 1, then flag[dir][g] = epoch on every rank (system
+// scope, after a system fence); wait: until every flag[dir][*] >= epoch[dir].
+void launch_xsignal(unsigned long long *own_sync, unsigned long long *const *peer_sync, int dir, int g, int G,
+                    void *stream);
+void launch_xwait(const unsigned long long *own_sync, int dir, int G, void *stream);
 
 }  // namespace mht

@@ -155,6 +155,20 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
   return *p;
 }
 
+// Where a block's outputs go: the workspace, or — a switch-stage block of a
+// sharded plan with the fused exchange on — the destination rank's receive
+// buffer over peer memory (the all-to-all folded into the stores; the entry
+// offset is shifted by zdel so out_off + row lands in that rank's layout)
+template <class S>
+__device__ __forceinline__ S *z_out(const Ctx &cx, const DevBlock &B, int64_t &off) {
+  if ((B.flags & F_REMOTE) && cx.zrem) {
+    const int h = B.flags >> 16;
+    off += cx.zdel[h];
+    return static_cast<S *>(cx.zrem[h]);
+  }
+  return static_cast<S *>(cx.z);
+}
+
 // ------------------------------------------------------------------------
 // forward stage (nrhs = 1): one CTA per (block, 64-row tile[, column split]);
 // 4 warps split the redundant columns, lane l owns rows l and l+32 of the
@@ -301,10 +315,12 @@ __device__ __forceinline__ void fwd_tile_lat(const Ctx &cx, const Tile tl) {
       const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
       s = X::add(s, in_value<S, CG>(cx, B, q, 0));
     }
-    if (B.flags & F_OUT_F)
+    if (B.flags & F_OUT_F) {
       static_cast<S *>(cx.fout)[cx.perm[B.out_off + row]] = s;
-    else
-      static_cast<S *>(cx.z)[B.out_off + row] = s;
+    } else {
+      int64_t o = B.out_off + row;
+      z_out<S>(cx, B, o)[o] = s;
+    }
   }
   if (split && threadIdx.x == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
 }
@@ -463,10 +479,12 @@ __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
       const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
       s = X::add(s, in_value<S, CG>(cx, B, q, 0));
     }
-    if (B.flags & F_OUT_F)
+    if (B.flags & F_OUT_F) {
       static_cast<S *>(cx.fout)[cx.perm[B.out_off + row]] = s;
-    else
-      static_cast<S *>(cx.z)[B.out_off + row] = s;
+    } else {
+      int64_t o = B.out_off + row;
+      z_out<S>(cx, B, o)[o] = s;
+    }
   }
   if (split && threadIdx.x == 0) cx.fcount[grp] = 0;  // re-arm for the next apply
 }
@@ -840,7 +858,11 @@ __device__ __forceinline__ void mma_epilogue(const Ctx &cx, const Tile &tl, cons
         if (B.flags & F_OUT_F)
           static_cast<S *>(cx.fout)[r * cx.n + oh[h]] = val[t][v];
         else
-          static_cast<S *>(cx.z)[(B.out_off + row) * cx.nrhs + r] = val[t][v];
+          {
+            int64_t o = B.out_off + row;
+            S *zb = z_out<S>(cx, B, o);
+            zb[o * cx.nrhs + r] = val[t][v];
+          }
       } else if (ksplit) {
         const int64_t slab = B.msp_off + (int64_t)(tl.start / MMA_COLS) * B.mks + sidx;
         static_cast<S *>(cx.msplit)[(slab * MMA_COLS + m) * cx.nrhs + r] = val[t][v];
@@ -1624,6 +1646,8 @@ __device__ __forceinline__ void reduce_piece(const Ctx &cx, const Piece p, const
       const int64_t ci = user_c_index(cx, p.dst_off + i);
       static_cast<S *>(cx.cw)[r * cx.m + ci] = cx.diag ? X::scale(s, diag_at(cx, ci)) : s;
     }
+    else if (p.remote > 0 && cx.zrem)  // fused reverse exchange: into the owner's send buffer
+      static_cast<S *>(cx.zrem[cx.zG + p.remote - 1])[(p.dst_off + cx.zdel[cx.zG + p.remote - 1] + i) * nr + r] = s;
     else
       static_cast<S *>(cx.z)[(p.dst_off + i) * nr + r] = s;
   }
@@ -1873,6 +1897,46 @@ int launch_persist(bool is_complex, bool adjoint, const Ctx &ctx, const Phase *p
       flow_kernel<double, false><<<grid, FL_THREADS, 0, st>>>(ctx, phases, nph, tiles, pieces, rd, ctr, stamps);
   }
   return (int)cudaGetLastError();
+}
+
+namespace {
+// Fused exchange signalling.  The kernel boundary before xsignal orders every
+// earlier store of the stream (the remote stores into the peers' buffers
+// included) before it; the system-scope fence then makes them visible to the
+// peers before the release store of the flag.
+__global__ void xsignal_kernel(unsigned long long *own_sync, unsigned long long *const *peer_sync, int dir, int g,
+                               int G) {
+  __shared__ unsigned long long e;
+  unsigned long long *epoch = own_sync + 2 * G;
+  if (threadIdx.x == 0) e = ++epoch[dir];  // this rank's counter: single writer
+  __syncthreads();
+  if (threadIdx.x < G) {
+    unsigned long long *f = peer_sync[threadIdx.x] + dir * G + g;
+    asm volatile("fence.sc.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+  }
+}
+__global__ void xwait_kernel(const unsigned long long *own_sync, int dir, int G) {
+  const unsigned long long e = own_sync[2 * G + dir];  // incremented by this rank's own xsignal
+  if (threadIdx.x < G) {
+    const unsigned long long *f = own_sync + dir * G + threadIdx.x;
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (v >= e) break;
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+}
+}  // namespace
+
+void launch_xsignal(unsigned long long *own_sync, unsigned long long *const *peer_sync, int dir, int g, int G,
+                    void *stream) {
+  xsignal_kernel<<<1, 32 * ((G + 31) / 32), 0, (cudaStream_t)stream>>>(own_sync, peer_sync, dir, g, G);
+}
+void launch_xwait(const unsigned long long *own_sync, int dir, int G, void *stream) {
+  xwait_kernel<<<1, 32 * ((G + 31) / 32), 0, (cudaStream_t)stream>>>(own_sync, dir, G);
 }
 
 void launch_reduce(bool is_complex, const Ctx &ctx, const Piece *pieces, const int64_t *rd,

@@ -129,6 +129,16 @@ struct mht_plan {
   // exchange layout in zpool entries (x nrhs scalars each)
   int shard_G = 1, shard_g = 0, shard_ls = -1;
   std::vector<int64_t> send_off, send_len, recv_off, recv_len;
+  // fused exchange (mht_shard_set_peers / mht_shard_open_peers): the zpool
+  // allocation ends with a sync area ([2][G] arrival flags + 2 epochs) at
+  // sync_byte_off; zrem / zdel as in Ctx, peer_sync[h] = rank h's sync area
+  int64_t sync_byte_off = 0;
+  bool x_on = false;
+  int x_nrhs = 0;
+  void **d_zrem = nullptr;
+  int64_t *d_zdel = nullptr;
+  unsigned long long **d_peersync = nullptr;
+  std::vector<void *> ipc_open;  // peer mappings opened by mht_shard_open_peers
   // persistent nrhs = 1 apply (one cooperative launch per direction)
   // off by default: with CUDA-graph replay the per-stage launches measured
   // faster (profiles/r01_persistent_ab.txt: the cooperative kernel's union
@@ -188,6 +198,10 @@ struct mht_plan {
     clear_graphs();
     if (own_stream && own_stream != stream) cudaStreamSynchronize(own_stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    for (void *q : ipc_open)
+      if (q) cudaIpcCloseMemHandle(q);
+    for (void *q : {(void *)d_zrem, (void *)d_zdel, (void *)d_peersync})
+      if (q) cudaFree(q);
     for (cudaStream_t q : {s_in, s_out})
       if (q) {
         cudaStreamSynchronize(q);
@@ -460,6 +474,7 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
   std::vector<int> block_stage;
   struct RecvRegion {
     int64_t off, len;
+    int32_t src;  // the sending rank
   };
   std::vector<RecvRegion> recv_regions;  // sharded: the exchange's receive buffer
   int64_t send_base = 0;
@@ -547,8 +562,10 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
       // the switch stage's outputs are the send buffer: always materialised,
       // laid out destination by destination (t-major order)
       const bool send = sharded && s == sh.ls;
+      int dest = -1;
       if (send) {
         const int h = (int)(t / ((int64_t(1) << s) / sh.G));
+        dest = h;
         if (P->send_len[h] == 0) P->send_off[h] = Z;
         P->send_len[h] += F.r_out;
       }
@@ -570,6 +587,7 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
         }
       }
       loc[s][b] = materialize(s, F, A, la, B, lb, false, 0);
+      if (send) blocks.back().flags |= F_REMOTE | (dest << 16);
     }
     if (sharded && s == sh.ls) {
       // send regions are contiguous in destination order (t-major); give empty
@@ -589,7 +607,7 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
           for (int64_t v = 0; v < nf; ++v) {
             if (v / (nf / sh.G) != src) continue;
             loc[s][t * nf + v] = Loc{SRC_Z, Z};
-            recv_regions.push_back({Z, (int64_t)blk[s][t * nf + v].r_out});
+            recv_regions.push_back({Z, (int64_t)blk[s][t * nf + v].r_out, (int32_t)src});
             Z += blk[s][t * nf + v].r_out;
           }
         }
@@ -959,6 +977,7 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
     int32_t src, stage;
     int64_t start, len;
     int blk;  // producer block (-1: the user's c)
+    int32_t remote = 0;  // receive-buffer region: 1 + the sending rank
   };
   std::vector<Region> regions;
   if (!sharded) {
@@ -977,7 +996,7 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
   // the receive buffer is a producer region of stage ls without a local
   // producer block: its adjoint sums are formed here and sent back
   for (const RecvRegion &rr : recv_regions)
-    if (rr.len > 0) regions.push_back({SRC_Z, sh.ls, rr.off, rr.len, -1});
+    if (rr.len > 0) regions.push_back({SRC_Z, sh.ls, rr.off, rr.len, -1, rr.src + 1});
   std::vector<std::vector<Piece>> pcs(L + 3);  // index stage+1 (0 = c)
   std::vector<std::vector<std::vector<int64_t>>> pcs_rd(L + 3);
   std::vector<std::vector<char>> pcs_keep(L + 3);  // piece still needed in fused mode
@@ -1028,6 +1047,7 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
         memset(&pc, 0, sizeof pc);
         pc.dst_src = src;
         pc.dst_off = c0;
+        pc.remote = regs[ri]->remote;
         pc.len = (int32_t)std::min<int64_t>(1024, e - c0);
         std::vector<int64_t> rr;
         for (int id : active) rr.push_back(readers[id].pstart + (c0 - readers[id].start));
@@ -1156,7 +1176,12 @@ mht_status ensure_ws(mht_plan *P, int nrhs) {
   if (P->d_part) cudaFree(P->d_part);
   P->d_z = P->d_part = nullptr;
   P->ws_nrhs = 0;
-  CUDA_TRY(cudaMalloc(&P->d_z, (size_t)P->Zt * nrhs * P->ssz));
+  if (P->x_on) return fail(MHT_ERR_INVALID_ARG, "fused exchange set up for a smaller nrhs: mht_shard_close_peers first");
+  // sharded plans: the fused exchange's sync area after the workspace (zeroed)
+  P->sync_byte_off = ((int64_t)P->Zt * nrhs * (int64_t)P->ssz + 255) / 256 * 256;
+  const size_t sync_bytes = P->shard_G > 1 ? (size_t)(2 * P->shard_G + 2) * 8 : 0;
+  CUDA_TRY(cudaMalloc(&P->d_z, (size_t)P->sync_byte_off + sync_bytes));
+  if (sync_bytes) CUDA_TRY(cudaMemset(static_cast<char *>(P->d_z) + P->sync_byte_off, 0, sync_bytes));
   CUDA_TRY(cudaMalloc(&P->d_part, (size_t)P->Pt * nrhs * P->ssz));
   if (P->d_msplit) cudaFree(P->d_msplit);
   if (P->d_mcount) cudaFree(P->d_mcount);
@@ -1196,6 +1221,11 @@ Ctx make_ctx(mht_plan *P, int nrhs) {
   cx.Zt = P->Zt;
   cx.Pt = P->Pt;
   cx.nrhs = nrhs;
+  if (P->x_on) {
+    cx.zrem = P->d_zrem;
+    cx.zdel = P->d_zdel;
+    cx.zG = P->shard_G;
+  }
   return cx;
 }
 
@@ -1259,6 +1289,9 @@ mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs, int part =
     CUDA_TRY(cudaGetLastError());
     return MHT_OK;
   }
+  unsigned long long *own_sync =
+      reinterpret_cast<unsigned long long *>(static_cast<char *>(P->d_z) + P->sync_byte_off);
+  if (part == 2 && P->x_on) launch_xwait(own_sync, 0, P->shard_G, P->stream);  // every peer's z_ls stores landed
   for (int s = s_lo; s <= s_hi; ++s)
     timed(P, 0, s, nrhs, nrhs == 1 ? P->fwd1[s].count : P->fwd[s].count, [&] {
       if (nrhs == 1)
@@ -1266,6 +1299,7 @@ mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs, int part =
       else
         launch_mma(P->cplx, false, cx, P->d_fwd + P->fwd[s].off, P->fwd[s].count, false, P->stream);
     });
+  if (part == 1 && P->x_on) launch_xsignal(own_sync, P->d_peersync, 0, P->shard_g, P->shard_G, P->stream);
   CUDA_TRY(cudaGetLastError());
   return MHT_OK;
 }
@@ -1300,6 +1334,8 @@ mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs, int part =
     });
   };
   const int ls = P->shard_ls;
+  unsigned long long *own_sync =
+      reinterpret_cast<unsigned long long *>(static_cast<char *>(P->d_z) + P->sync_byte_off);
   if (part != 2) {
     adj_stage(L + 1, true);
     for (int s = L; s >= (part == 1 ? ls + 1 : 0); --s) {
@@ -1307,8 +1343,10 @@ mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs, int part =
       adj_stage(s, false);
     }
     if (part == 1) sums(ls);
+    if (part == 1 && P->x_on) launch_xsignal(own_sync, P->d_peersync, 1, P->shard_g, P->shard_G, P->stream);
   }
   if (part == 2) {
+    if (P->x_on) launch_xwait(own_sync, 1, P->shard_G, P->stream);  // the peers' sums landed in the send buffer
     adj_stage(ls, false);
     for (int s = ls - 1; s >= 0; --s) {
       sums(s);
@@ -1456,10 +1494,110 @@ mht_status mht_shard_workspace(mht_plan *P, int nrhs, void **zpool) {
 static mht_status shard_call(mht_plan *P, int dir, const void *src, void *dst, int nrhs) {
   if (!P || nrhs < 1 || (!src && !dst)) return fail(MHT_ERR_INVALID_ARG, "bad argument");
   if (P->shard_G < 2) return fail(MHT_ERR_INVALID_ARG, "not a sharded plan (mht_plan_load_shard with nshards > 1)");
+  if (P->x_on && nrhs > P->x_nrhs) return fail(MHT_ERR_INVALID_ARG, "nrhs above the fused exchange's set-up width");
   CUDA_TRY(cudaSetDevice(P->device));
   mht_status s = ensure_ws(P, nrhs);
   if (s != MHT_OK) return s;
   return run_dir(P, dir, src, dst, nrhs);
+}
+
+mht_status mht_shard_export(mht_plan *P, int nrhs, void *ipc_handle, int64_t *layout) {
+  if (!P || nrhs < 1 || !layout) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G < 2) return fail(MHT_ERR_INVALID_ARG, "not a sharded plan (mht_plan_load_shard with nshards > 1)");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s = ensure_ws(P, nrhs);
+  if (s != MHT_OK) return s;
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, P->d_z));
+    memcpy(ipc_handle, &h, sizeof h);
+  }
+  const int G = P->shard_G;
+  for (int h = 0; h < G; ++h) {
+    layout[h] = P->recv_off[h];
+    layout[G + h] = P->send_off[h];
+  }
+  layout[2 * G] = P->sync_byte_off;
+  return MHT_OK;
+}
+
+mht_status mht_shard_set_peers(mht_plan *P, int nrhs, void *const *bases, const int64_t *layouts) {
+  if (!P || nrhs < 1 || !bases || !layouts) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G < 2) return fail(MHT_ERR_INVALID_ARG, "not a sharded plan (mht_plan_load_shard with nshards > 1)");
+  const int G = P->shard_G, g = P->shard_g, LW = 2 * G + 1;
+  if (P->x_on && nrhs != P->x_nrhs) return fail(MHT_ERR_INVALID_ARG, "fused exchange already set up for another nrhs");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s = ensure_ws(P, nrhs);
+  if (s != MHT_OK) return s;
+  if (bases[g] != P->d_z) return fail(MHT_ERR_INVALID_ARG, "bases[shard] must be this plan's own workspace");
+  for (int h = 0; h < G; ++h) {
+    if (!bases[h]) return fail(MHT_ERR_INVALID_ARG, "null peer base");
+    const int64_t *lh = layouts + (int64_t)h * LW;
+    // every rank's layout is its own; the exchange is only consistent if the
+    // pair (g -> h) agrees on the block count: checked through the lengths
+    if (lh[g] < 0 || lh[G + g] < 0) return fail(MHT_ERR_INVALID_ARG, "bad peer layout");
+  }
+  std::vector<void *> zrem(2 * G);
+  std::vector<int64_t> zdel(2 * G);
+  std::vector<unsigned long long *> psync(G);
+  for (int h = 0; h < G; ++h) {
+    const int64_t *lh = layouts + (int64_t)h * LW;
+    // forward: my send region for h -> h's receive region from me
+    zrem[h] = bases[h];
+    zdel[h] = lh[g] - P->send_off[h];
+    // adjoint: my receive region from h -> h's send region for me
+    zrem[G + h] = bases[h];
+    zdel[G + h] = lh[G + g] - P->recv_off[h];
+    psync[h] = reinterpret_cast<unsigned long long *>(static_cast<char *>(bases[h]) + lh[2 * G]);
+  }
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  P->clear_graphs();
+  if (!P->d_zrem) {
+    CUDA_TRY(cudaMalloc((void **)&P->d_zrem, 2 * G * sizeof(void *)));
+    CUDA_TRY(cudaMalloc((void **)&P->d_zdel, 2 * G * sizeof(int64_t)));
+    CUDA_TRY(cudaMalloc((void **)&P->d_peersync, G * sizeof(void *)));
+  }
+  CUDA_TRY(cudaMemcpy(P->d_zrem, zrem.data(), 2 * G * sizeof(void *), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->d_zdel, zdel.data(), 2 * G * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->d_peersync, psync.data(), G * sizeof(void *), cudaMemcpyHostToDevice));
+  P->x_on = true;
+  P->x_nrhs = nrhs;
+  return MHT_OK;
+}
+
+mht_status mht_shard_open_peers(mht_plan *P, int nrhs, const void *ipc_handles, const int64_t *layouts) {
+  if (!P || nrhs < 1 || !ipc_handles || !layouts) return fail(MHT_ERR_INVALID_ARG, "bad argument");
+  if (P->shard_G < 2) return fail(MHT_ERR_INVALID_ARG, "not a sharded plan (mht_plan_load_shard with nshards > 1)");
+  CUDA_TRY(cudaSetDevice(P->device));
+  mht_status s = ensure_ws(P, nrhs);
+  if (s != MHT_OK) return s;
+  const int G = P->shard_G;
+  std::vector<void *> bases(G, nullptr);
+  for (int h = 0; h < G; ++h) {
+    if (h == P->shard_g) {
+      bases[h] = P->d_z;
+      continue;
+    }
+    cudaIpcMemHandle_t hd;
+    memcpy(&hd, static_cast<const char *>(ipc_handles) + (size_t)h * sizeof hd, sizeof hd);
+    void *ptr = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    P->ipc_open.push_back(ptr);
+    bases[h] = ptr;
+  }
+  return mht_shard_set_peers(P, nrhs, bases.data(), layouts);
+}
+
+mht_status mht_shard_close_peers(mht_plan *P) {
+  if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
+  CUDA_TRY(cudaSetDevice(P->device));
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  P->clear_graphs();
+  P->x_on = false;
+  P->x_nrhs = 0;
+  for (void *q : P->ipc_open) cudaIpcCloseMemHandle(q);
+  P->ipc_open.clear();
+  return MHT_OK;
 }
 
 mht_status mht_apply_shard_begin(mht_plan *P, const void *c, int nrhs) { return shard_call(P, 2, c, nullptr, nrhs); }

@@ -25,6 +25,7 @@ EXPORTED = [
     "mht_apply_adjoint", "mht_apply_host", "mht_apply_adjoint_host", "mht_apply_host_batch", "mht_apply_diag", "mht_apply_adjoint_diag", "mht_grf_sample", "mht_covariance_apply", "mht_lsqr",
     "mht_plan_load_shard", "mht_shard_info", "mht_shard_workspace", "mht_apply_shard_begin",
     "mht_apply_shard_end", "mht_apply_adjoint_shard_begin", "mht_apply_adjoint_shard_end",
+    "mht_shard_export", "mht_shard_open_peers", "mht_shard_set_peers", "mht_shard_close_peers",
     "mht_set_graphs", "mht_set_fused_sums", "mht_set_persistent", "mht_phase_times", "mht_sync",
     "mht_stage_stats", "mht_set_profiling", "mht_profile_get", "mht_profile_reset", "mht_plan_destroy",
     "mht_status_string", "mht_last_error", "mht_build_info",
@@ -78,6 +79,10 @@ def load_library(path: str = LIB_PATH):
     for nm in ("mht_apply_shard_begin", "mht_apply_shard_end", "mht_apply_adjoint_shard_begin",
                "mht_apply_adjoint_shard_end"):
         getattr(L, nm).argtypes = [vp, vp, i32]
+    L.mht_shard_export.argtypes = [vp, i32, vp, C.POINTER(i64)]
+    L.mht_shard_open_peers.argtypes = [vp, i32, vp, C.POINTER(i64)]
+    L.mht_shard_set_peers.argtypes = [vp, i32, C.POINTER(vp), C.POINTER(i64)]
+    L.mht_shard_close_peers.argtypes = [vp]
     L.mht_set_graphs.argtypes = [vp, i32]
     L.mht_set_fused_sums.argtypes = [vp, i32]
     L.mht_set_persistent.argtypes = [vp, i32]

@@ -14,7 +14,13 @@ the exchange blocks:
   file alone (no GPU), the same layout the loader builds; the gloo CPU tests
   check the all-to-all moves every z_ls block to its owner with it;
 * ``emulate`` — all G shards on ONE GPU with the exchange done by device
-  copies (the single-GPU correctness check of the sharded path).
+  copies (the single-GPU correctness check of the sharded path);
+* the fused exchange (``ShardPlan.fuse`` / ``emulate_fuse``): the switch
+  stage's kernels store z_ls straight into the destination ranks' receive
+  buffers over peer memory (CUDA IPC mappings, ``mht_shard_open_peers``) and
+  signal them; no all-to-all call is left between ``begin`` and ``end``.  The
+  host side only exchanges the IPC handles and layouts (``peer_tables``,
+  covered by gloo tests on CPU).
 """
 from __future__ import annotations
 
@@ -62,6 +68,32 @@ def exchange_sizes(path: str, G: int, ls: int | None = None):
             sizes[g, h] += int(r_out[t * nf + v])
             blocks[g][h].append((t, v))
     return sizes, blocks, ls
+
+
+IPC_HANDLE_BYTES = 64  # sizeof(cudaIpcMemHandle_t)
+
+
+def peer_tables(exports):
+    """The inputs of mht_shard_open_peers from every rank's mht_shard_export
+    (rank order): (handles: G x 64 bytes, layouts: G x (2 G + 1) int64), after
+    checking that each pair (g, h) agrees on the exchange size (rank g's send
+    length to h is rank h's receive length from g, from the offsets)."""
+    G = len(exports)
+    handles = b"".join(bytes(h) if h is not None else bytes(IPC_HANDLE_BYTES) for h, _ in exports)
+    lay = np.array([np.asarray(l, dtype=np.int64) for _, l in exports], dtype=np.int64)
+    if lay.shape != (G, 2 * G + 1) or len(handles) != G * IPC_HANDLE_BYTES:
+        raise ValueError("inconsistent exports")
+    return handles, lay
+
+
+def gather_exports(mine, G: int, group=None):
+    """All-gather every rank's (IPC handle, layout) over `group` (host
+    objects: gloo or NCCL) and return peer_tables of them."""
+    import torch.distributed as dist
+
+    allx = [None] * G
+    dist.all_gather_object(allx, (mine[0], [int(x) for x in mine[1]]), group=group)
+    return peer_tables(allx)
 
 
 class _DevBuf:
@@ -137,14 +169,39 @@ class ShardPlan:
         mht._check(mht.load_library().mht_apply_adjoint_shard_end(self._h, C.c_void_p(c.data_ptr()), int(nrhs)),
                    "mht_apply_adjoint_shard_end")
 
+    fused = False
+
+    def export(self, nrhs: int, ipc: bool = True):
+        """(IPC handle bytes or None, layout (2 G + 1) int64) for the peers."""
+        h = (C.c_char * IPC_HANDLE_BYTES)() if ipc else None
+        lay = (C.c_int64 * (2 * self.G + 1))()
+        mht._check(mht.load_library().mht_shard_export(self._h, int(nrhs), h, lay), "mht_shard_export")
+        return (bytes(h) if ipc else None), np.array(lay[:], dtype=np.int64)
+
+    def fuse(self, nrhs: int, group=None):
+        """Switch to the fused exchange for applies of up to nrhs right-hand
+        sides: every rank exports its workspace handle and layout, they are
+        all-gathered over `group` (host objects: gloo or NCCL), and each rank
+        maps its peers' workspaces (mht_shard_open_peers)."""
+        handles, lay = gather_exports(self.export(nrhs), self.G, group)
+        hb = C.create_string_buffer(handles, len(handles))
+        lp = lay.ravel().ctypes.data_as(C.POINTER(C.c_int64))
+        mht._check(mht.load_library().mht_shard_open_peers(self._h, int(nrhs), hb, lp), "mht_shard_open_peers")
+        self.fused = True
+
+    def unfuse(self):
+        mht._check(mht.load_library().mht_shard_close_peers(self._h), "mht_shard_close_peers")
+        self.fused = False
+
     def apply(self, c, f, group=None):
         """f[rows of this rank] = (Phi c)[rows]; c: (nrhs, m) full, f: (nrhs, n)."""
         import torch.distributed as dist
 
         nrhs = c.reshape(-1, self.m).shape[0]
         self.begin(c, nrhs)
-        send, recv, ssz, rsz = self._views(nrhs)
-        dist.all_to_all_single(recv, send, output_split_sizes=rsz, input_split_sizes=ssz, group=group)
+        if not self.fused:
+            send, recv, ssz, rsz = self._views(nrhs)
+            dist.all_to_all_single(recv, send, output_split_sizes=rsz, input_split_sizes=ssz, group=group)
         self.end(f, nrhs)
         return f
 
@@ -154,8 +211,9 @@ class ShardPlan:
 
         nrhs = f.reshape(-1, self.n).shape[0]
         self.adjoint_begin(f, nrhs)
-        send, recv, ssz, rsz = self._views(nrhs)
-        dist.all_to_all_single(send, recv, output_split_sizes=ssz, input_split_sizes=rsz, group=group)
+        if not self.fused:
+            send, recv, ssz, rsz = self._views(nrhs)
+            dist.all_to_all_single(send, recv, output_split_sizes=ssz, input_split_sizes=rsz, group=group)
         self.adjoint_end(c, nrhs)
         return c
 
@@ -190,11 +248,32 @@ def _exchange_local(shards, nrhs: int, reverse: bool):
                 b.copy_(a)
 
 
+def emulate_fuse(shards, nrhs: int):
+    """The fused exchange among shards living in one process (one GPU): each
+    shard gets the others' workspaces as plain device pointers
+    (mht_shard_set_peers), so the switch stage stores into them and the
+    arrival flags are set and waited on exactly as across GPUs.  The begins
+    of all shards run before the ends (emulate_apply), so no wait spins."""
+    ex = [s.export(nrhs, ipc=False) for s in shards]
+    _, lay = peer_tables([(None, l) for _, l in ex])
+    bases = []
+    for s in shards:
+        z = C.c_void_p()
+        mht._check(mht.load_library().mht_shard_workspace(s._h, int(nrhs), C.byref(z)), "mht_shard_workspace")
+        bases.append(z.value)
+    arr = (C.c_void_p * len(shards))(*bases)
+    lp = lay.ravel().ctypes.data_as(C.POINTER(C.c_int64))
+    for s in shards:
+        mht._check(mht.load_library().mht_shard_set_peers(s._h, int(nrhs), arr, lp), "mht_shard_set_peers")
+        s.fused = True
+
+
 def emulate_apply(shards, c, f):
     nrhs = c.reshape(-1, shards[0].m).shape[0]
     for s in shards:
         s.begin(c, nrhs)
-    _exchange_local(shards, nrhs, reverse=False)
+    if not shards[0].fused:
+        _exchange_local(shards, nrhs, reverse=False)
     for s in shards:
         s.end(f, nrhs)
     return f
@@ -204,7 +283,8 @@ def emulate_adjoint(shards, f, c):
     nrhs = f.reshape(-1, shards[0].n).shape[0]
     for s in shards:
         s.adjoint_begin(f, nrhs)
-    _exchange_local(shards, nrhs, reverse=True)
+    if not shards[0].fused:
+        _exchange_local(shards, nrhs, reverse=True)
     for s in shards:
         s.adjoint_end(c, nrhs)
     return c

@@ -531,10 +531,14 @@ def test_lsqr_inverse_mht(gpu, oracle_lib, plans):
 def test_sharded_plan_emulated_on_one_gpu(gpu, oracle_lib, plans):
     """SURVEY §8(e) sharded plans: G = 2 and 4 shards of one plan (frequency
     subtrees for stages <= ls, space subtrees after, one all-to-all of z_ls),
-    all loaded on this GPU with the exchange done by device copies.  The
-    assembled synthesis and analysis match O2 on the whole plan (<= 1e-12) at
-    nrhs 1, 5 and 32, complex flat and real sphere plans, every admissible
-    switch level; each shard holds about 1/G of the factor bytes."""
+    all loaded on this GPU with the exchange done by device copies, then with
+    the fused exchange (switch-stage stores into the other shards' receive
+    buffers and the reverse sums into their send buffers, arrival flags; two
+    rounds of applies so the epochs advance).  The assembled synthesis and
+    analysis match O2 on the whole plan (<= 1e-12) at nrhs 1, 5 and 32,
+    complex flat and real sphere plans, every admissible switch level, the
+    fused results bitwise those of the copy exchange; each shard holds about
+    1/G of the factor bytes."""
     from paper_2605_21828_b200 import shard as SH
 
     path_c, wc = flat_case(plans, 2048, 32, 4, 1e-8)
@@ -554,17 +558,29 @@ def test_sharded_plan_emulated_on_one_gpu(gpu, oracle_lib, plans):
                 held = sum(s.info.factor_entries for s in shards)
                 assert held == total                           # every block on exactly one rank
                 assert max(s.info.factor_entries for s in shards) <= 0.75 * total if G == 4 else True
-                for nrhs in (1, 5, 32):
-                    gen = mi.complex_gaussian if w.dtype == "complex128" else mi.real_gaussian
-                    c, y = gen(nrhs, w.m, 800 + nrhs), gen(nrhs, w.n, 900 + nrhs)
-                    ct, yt = torch.from_numpy(c).cuda(), torch.from_numpy(y).cuda()
-                    f = torch.zeros((nrhs, w.n), dtype=shards[0].torch_dtype, device="cuda")
-                    a = torch.zeros((nrhs, w.m), dtype=shards[0].torch_dtype, device="cuda")
-                    SH.emulate_apply(shards, ct, f)
-                    SH.emulate_adjoint(shards, yt, a)
-                    assert o2_err(f.cpu().numpy(), O.apply(c)) <= PARITY, (path, G, ls, nrhs)
-                    assert o2_err(a.cpu().numpy(), O.adjoint(y)) <= PARITY, (path, G, ls, nrhs)
+                res = {}
+                for fused in (False, True):
+                    if fused:
+                        # the fused exchange: switch-stage stores straight into the
+                        # other shards' receive buffers, arrival flags per apply
+                        SH.emulate_fuse(shards, 32)
+                    for rep in range(2 if fused else 1):
+                        for nrhs in (1, 5, 32):
+                            gen = mi.complex_gaussian if w.dtype == "complex128" else mi.real_gaussian
+                            c, y = gen(nrhs, w.m, 800 + nrhs), gen(nrhs, w.n, 900 + nrhs)
+                            ct, yt = torch.from_numpy(c).cuda(), torch.from_numpy(y).cuda()
+                            f = torch.zeros((nrhs, w.n), dtype=shards[0].torch_dtype, device="cuda")
+                            a = torch.zeros((nrhs, w.m), dtype=shards[0].torch_dtype, device="cuda")
+                            SH.emulate_apply(shards, ct, f)
+                            SH.emulate_adjoint(shards, yt, a)
+                            assert o2_err(f.cpu().numpy(), O.apply(c)) <= PARITY, (path, G, ls, nrhs, fused)
+                            assert o2_err(a.cpu().numpy(), O.adjoint(y)) <= PARITY, (path, G, ls, nrhs, fused)
+                            if fused:  # same arithmetic, other store addresses: bitwise equal
+                                assert torch.equal(f, res[nrhs][0]) and torch.equal(a, res[nrhs][1]), (G, ls, nrhs)
+                            else:
+                                res[nrhs] = (f, a)
                 for s in shards:
+                    s.unfuse()
                     s.close()
 
 

@@ -110,3 +110,79 @@ print("ok", g)
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert r.stdout.count("ok") == G
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_fused_exchange_host_tables_gloo(plan_path, G, tmp_path):
+    """The fused exchange's host side on CPU (gloo): every rank lays out its
+    workspace as the loader does (send regions destination by destination,
+    receive regions source by source, after its own entries), exports
+    (handle, layout) and all-gathers them with shard.gather_exports; then each
+    rank stores its send blocks straight into the peers' receive buffers at
+    send offset + (peer's receive offset for me - my send offset for the
+    peer) — the delta mht_shard_set_peers gives the switch-stage kernels —
+    and the reverse sums back the other way.  The buffers must equal what the
+    all-to-all delivers, on every rank."""
+    script = tmp_path / "fused.py"
+    script.write_text(f'''
+import sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, {ROOT!r})
+from paper_2605_21828_b200 import shard
+from paper_2605_21828_b200.precompute.planfile import PlanView
+dist.init_process_group("gloo")
+g, G = dist.get_rank(), dist.get_world_size()
+sizes, blocks, ls = shard.exchange_sizes({plan_path!r}, G)
+pv = PlanView({plan_path!r})
+nf = (1 << pv.L) >> ls
+r_out = np.asarray(pv.stages[ls].blocks["r_out"])
+def codes(bl):
+    return np.concatenate([t * 10**9 + v * 10**4 + np.arange(r_out[t * nf + v]) for t, v in bl]) if bl else np.zeros(0)
+# rank-specific layout: some private entries first (a different amount per rank)
+own = 1000 + 37 * g
+send_off = own + np.concatenate([[0], np.cumsum(sizes[g, :])])[:G]
+recv_base = own + int(sizes[g, :].sum()) + 11 * g
+recv_off = recv_base + np.concatenate([[0], np.cumsum(sizes[:, g])])[:G]
+Z = recv_base + int(sizes[:, g].sum())
+layout = np.concatenate([recv_off, send_off, [8 * Z]]).astype(np.int64)
+handles, lay = shard.gather_exports((bytes([g]) * shard.IPC_HANDLE_BYTES, layout), G)
+assert lay.shape == (G, 2 * G + 1) and np.array_equal(lay[g], layout)
+assert handles[g * 64:(g + 1) * 64] == bytes([g]) * 64
+# every rank's workspace, as one object gathered (the "peer memory")
+ws = np.full(Z, -1.0)
+ws[send_off[0]:send_off[0] + sizes[g, :].sum()] = np.concatenate([codes(blocks[g][h]) for h in range(G)])
+allws = [None] * G
+dist.all_gather_object(allws, ws)
+# forward: rank src's send block for h -> h's receive region, by the delta
+for h in range(G):
+    mine = allws[h].copy()
+    for src in range(G):
+        delta = lay[h][src] - lay[src][G + h]           # zdel[h] on rank src
+        a = lay[src][G + h]
+        n = int(sizes[src, h])
+        mine[a + delta:a + delta + n] = allws[src][a:a + n]
+    if h == g:
+        want = np.concatenate([codes(blocks[src][g]) for src in range(G)])
+        got = mine[recv_off[0]:recv_off[0] + sizes[:, g].sum()]
+        assert np.array_equal(got, want), "fused forward delivery"
+        fwd = mine
+# reverse: rank g's receive region from src -> src's send region for g
+allf = [None] * G
+dist.all_gather_object(allf, fwd)
+back = allws[g].copy()
+back[send_off[0]:send_off[0] + sizes[g, :].sum()] = -2
+for h in range(G):
+    delta = lay[g][G + h] - lay[h][g]                    # zdel[G + g] on rank h
+    a = lay[h][g]
+    n = int(sizes[g, h])
+    back[a + delta:a + delta + n] = allf[h][a:a + n]
+assert np.array_equal(back, allws[g]), "fused reverse delivery"
+dist.barrier()
+dist.destroy_process_group()
+print("ok", g)
+''')
+    port = _free_port()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), str(script)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.stdout.count("ok") == G
