@@ -384,11 +384,6 @@ def main():
                 ms, nl = P.profile_get(kind_i, s_, r)
                 if nl:
                     row[str(s_)] = round(ms / args.steps, 4)
-            if r == 1 and kind in ("fwd", "adj"):
-                # persistent nrhs = 1 apply: per-phase times from the kernel's barrier stamps
-                for st_, kd_, ms_ in P.phase_times(0 if kind == "fwd" else 1):
-                    key = str(st_) if kd_ != 2 else f"sum{st_}"
-                    row[key] = round(ms_, 4)
             if kind == "sum":  # stage -1 (the final sums into c) = all - the per-stage ones
                 ms, nl = P.profile_get(kind_i, -1, r)
                 if nl:
@@ -413,8 +408,7 @@ def main():
     if dr == 1:
         alg = (coef_bytes + (w.m + w.n) * sb) / (dn / args.steps)        # bytes per launch (average)
         achieved = alg / (per_launch_ms / 1e3) / 1e9
-        kname = (f"persist_kernel {dkind} nrhs=1 (all stages in one cooperative launch)" if dn == args.steps
-                 else f"{dkind}_kernel nrhs=1")
+        kname = f"{dkind}_kernel nrhs=1"
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "frac_of_nominal_8TBs": achieved / 8000.0,
                 "traffic": traffic, "algorithmic_bytes_per_launch": alg,

@@ -266,23 +266,6 @@ mht_status mht_set_graphs(mht_plan *plan, int on);
  * Synchronises the plan's stream and drops captured graphs. */
 mht_status mht_set_fused_sums(mht_plan *plan, int on);
 
-/* nrhs = 1 execution mode.  on = 1: each apply is ONE cooperative
- * ("persistent") launch that walks every stage of the direction, CTAs pulling
- * tiles from per-stage work counters and meeting at a grid barrier between
- * stages.  on = 0 (default): one launch per stage (replayed as a CUDA graph),
- * which measured faster on B200.  Results are bitwise identical.  Multi-RHS
- * applies always launch per stage.
- * Synchronises the plan's stream and drops captured graphs. */
-mht_status mht_set_persistent(mht_plan *plan, int on);
-
-/* Per-phase device time of the last PROFILED persistent apply in direction
- * dir (0 = synthesis, 1 = analysis), from %globaltimer stamps taken at the
- * grid barriers.  Writes up to cap entries: ms[i], the plan stage of phase i
- * (-1 = the sums into c) and its kind (0 forward stage, 1 adjoint stage,
- * 2 group sums); *nphases = entries written (0 if none recorded).  Synchronises. */
-mht_status mht_phase_times(mht_plan *plan, int dir, double *ms, int32_t *stage, int32_t *kind, int cap,
-                           int *nphases);
-
 /* Block until the plan's stream is idle; returns MHT_ERR_CUDA on a fault
  * (the asynchronous error surface of the calls above). */
 mht_status mht_sync(mht_plan *plan);

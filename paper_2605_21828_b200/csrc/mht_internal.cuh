@@ -119,19 +119,6 @@ constexpr int ADJ_RCH = 1024;    // adjoint rows staged in smem per pass (most b
                                  // 256 / 512 measured 8% slower on c2, profiles/r01_adj_rch_ab.txt)
 constexpr int MMA_COLS = 64;     // redundant columns per multi-RHS adjoint tile
 
-// One phase of the one-launch nrhs = 1 apply (a stage's tiles or a list of
-// group-sum pieces); its units wait for the previous phase's done-counter.
-enum : int32_t { PH_FWD = 0, PH_ADJ = 1, PH_SUM = 2 };
-struct Phase {
-  int32_t kind;    // PH_FWD | PH_ADJ | PH_SUM
-  int32_t from_f;  // PH_ADJ: input is f through perm_x (leaf stage)
-  int32_t off;     // first tile / piece
-  int32_t count;   // tiles / pieces
-  int32_t stage;   // plan stage (-1: the sums into c)
-  int32_t pad;
-};
-
-
 // LSQR per-column state (device resident; mht_lsqr.cu)
 struct LsqrCol {
   double alpha, beta, rhobar, phibar, cs;
@@ -160,12 +147,6 @@ void launch_adj(bool is_complex, const Ctx &ctx, const Tile *tiles, int ntiles, 
 // adjoint uses 64-column tiles (adjm lists).
 void launch_mma(bool is_complex, bool adjoint, const Ctx &ctx, const Tile *tiles, int ntiles, bool in_from_f,
                 void *stream);
-// one-launch (dataflow) nrhs = 1 apply of one direction: returns a
-// cudaError_t value (0 = launched).  tiles: the forward (fwd1) or adjoint tile list.
-int launch_persist(bool is_complex, bool adjoint, const Ctx &ctx, const Phase *phases, int nph, const Tile *tiles,
-                   const Piece *pieces, const int64_t *rd, int *ctr, unsigned long long *stamps, int grid,
-                   void *stream);
-int persist_grid(bool is_complex);
 void launch_repack(const double *src, double *dst, const Repack *jobs, int njobs, void *stream);
 void launch_reduce(bool is_complex, const Ctx &ctx, const Piece *pieces, const int64_t *rd,
                    int npieces, void *stream);

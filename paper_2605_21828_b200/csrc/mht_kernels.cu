@@ -136,11 +136,7 @@ __device__ __forceinline__ double diag_at(const Ctx &cx, int64_t k) {
   return cx.diag_sqrt ? sqrt(d) : d;
 }
 
-// CG: read the workspace through L2 only (ld.global.cg).  The persistent
-// kernel writes and reads workspace in different phases of ONE launch, and L1
-// is not coherent: a line cached while reading one stage's z could be stale
-// for the next stage's entries that share it.
-template <class S, bool CG = false>
+template <class S>
 __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, int r) {
   const bool s1 = q >= B.seg_len[0];  // no dynamic indexing: keeps B in registers
   const int64_t off = s1 ? B.seg_off[1] + (q - B.seg_len[0]) : B.seg_off[0] + q;
@@ -150,9 +146,7 @@ __device__ __forceinline__ S in_value(const Ctx &cx, const DevBlock &B, int q, i
     const S v = static_cast<const S *>(cx.c)[r * cx.m + ci];
     return cx.diag ? Tr<S>::scale(v, diag_at(cx, ci)) : v;
   }
-  const S *p = static_cast<const S *>(cx.z) + off * cx.nrhs + r;           // workspace: RHS-fastest
-  if constexpr (CG) return Tr<S>::ldcg(p);
-  return *p;
+  return static_cast<const S *>(cx.z)[off * cx.nrhs + r];  // workspace: RHS-fastest
 }
 
 // Where a block's outputs go: the workspace, or — a switch-stage block of a
@@ -177,10 +171,9 @@ __device__ __forceinline__ S *z_out(const Ctx &cx, const DevBlock &B, int64_t &o
 // row sums to scratch and the last CTA of the group to arrive (atomic counter)
 // adds them in split order — deterministic, no float atomics.
 // ------------------------------------------------------------------------
-// CG: workspace reads through L2 only (the persistent kernel; see in_value)
 // PFD: the L2 prefetch runs this many batch rounds ahead (8: c1 107.6 -> 105.0 us,
 // c4 81.4 -> 79.9 us against 2; profiles/r02_fwd_variants_ab.txt)
-template <class S, bool CG, int PFD = 8>
+template <class S, int PFD = 8>
 __device__ __forceinline__ void fwd_tile_lat(const Ctx &cx, const Tile tl) {
   using X = Tr<S>;
   const DevBlock B = cx.blocks[tl.blk];
@@ -219,7 +212,7 @@ __device__ __forceinline__ void fwd_tile_lat(const Ctx &cx, const Tile tl) {
     if (jc > jbeg) __syncthreads();  // every warp is past its reads of the previous chunk
     for (int j = threadIdx.x; j < jn; j += FWD_THREADS) {
       const int q = red_iota ? jc + j : cx.idx[B.red_off + jc + j];
-      xs[j] = in_value<S, CG>(cx, B, q, 0);
+      xs[j] = in_value<S>(cx, B, q, 0);
     }
     __syncthreads();
     const int wb = warp * FB, we = jn;
@@ -313,7 +306,7 @@ __device__ __forceinline__ void fwd_tile_lat(const Ctx &cx, const Tile tl) {
     const int row = tl.start + i;
     if (row < B.n_skel) {
       const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
-      s = X::add(s, in_value<S, CG>(cx, B, q, 0));
+      s = X::add(s, in_value<S>(cx, B, q, 0));
     }
     if (B.flags & F_OUT_F) {
       static_cast<S *>(cx.fout)[cx.perm[B.out_off + row]] = s;
@@ -354,13 +347,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 7) fwd_lat_kernel(const Ctx cx, c
     }
   }
   pdl_wait();
-  fwd_tile_lat<S, false>(cx, tl);
+  fwd_tile_lat<S>(cx, tl);
 }
 
 // nrhs = 1 forward, streaming variant (stages of many waves): lane j of a
 // warp gathers x for its 32-column group, broadcast by shuffle, 8 columns'
 // loads in flight per step, 72 registers (7 CTAs per SM without the x buffer).
-template <class S, bool CG>
+template <class S>
 __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
   using X = Tr<S>;
   const DevBlock B = cx.blocks[tl.blk];
@@ -388,7 +381,7 @@ __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
     S xr = X::zero();
     if (j < jend) {
       const int q = (B.flags & F_RED_IOTA) ? j : cx.idx[B.red_off + j];
-      xr = in_value<S, CG>(cx, B, q, 0);
+      xr = in_value<S>(cx, B, q, 0);
     }
     const int jn = min(32, jend - j0);
     const S *col = T + (int64_t)j0 * ld;
@@ -477,7 +470,7 @@ __device__ __forceinline__ void fwd_tile(const Ctx &cx, const Tile tl) {
     const int row = tl.start + i;
     if (row < B.n_skel) {
       const int q = (B.flags & F_SKEL_IOTA) ? row : cx.idx[B.skel_off + row];
-      s = X::add(s, in_value<S, CG>(cx, B, q, 0));
+      s = X::add(s, in_value<S>(cx, B, q, 0));
     }
     if (B.flags & F_OUT_F) {
       static_cast<S *>(cx.fout)[cx.perm[B.out_off + row]] = s;
@@ -510,7 +503,7 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Ti
     }
   }
   pdl_wait();
-  fwd_tile<S, false>(cx, tl);
+  fwd_tile<S>(cx, tl);
 }
 
 // adjoint input z[i] of a block: f through perm_x (leaf stage), else the group
@@ -519,21 +512,16 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_kernel(const Ctx cx, const Ti
 // no separate reduction pass) or read from the zpool slot reduce_kernel wrote.
 // The fused sum adds the partials in the same (reader id) order as
 // reduce_kernel, so both paths are bitwise identical.
-template <class S, bool CG = false>
+template <class S>
 __device__ __forceinline__ S adj_in(const Ctx &cx, const DevBlock &B, int i, int r, bool from_f) {
   if (from_f) return static_cast<const S *>(cx.fin)[r * cx.n + cx.perm[B.out_off + i]];
   if (cx.fused && B.rd_cnt >= 0) {
     const S *part = static_cast<const S *>(cx.part);
     S s = Tr<S>::zero();
-    for (int k = 0; k < B.rd_cnt; ++k) {
-      const S *p = part + (cx.rdtab[B.rd_off + k] + i) * cx.nrhs + r;
-      s = Tr<S>::add(s, CG ? Tr<S>::ldcg(p) : *p);
-    }
+    for (int k = 0; k < B.rd_cnt; ++k) s = Tr<S>::add(s, part[(cx.rdtab[B.rd_off + k] + i) * cx.nrhs + r]);
     return s;
   }
-  const S *p = static_cast<const S *>(cx.z) + (B.out_off + i) * cx.nrhs + r;
-  if constexpr (CG) return Tr<S>::ldcg(p);
-  return *p;
+  return static_cast<const S *>(cx.z)[(B.out_off + i) * cx.nrhs + r];
 }
 
 // ------------------------------------------------------------------------
@@ -546,7 +534,7 @@ __device__ __forceinline__ S adj_in(const Ctx &cx, const DevBlock &B, int i, int
 // partial column sums to scratch and the last CTA of the group to arrive adds
 // them in split order (deterministic, no float atomics).
 // ------------------------------------------------------------------------
-template <class S, bool CG>
+template <class S>
 __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_f) {
   using X = Tr<S>;
   // columns per warp: 8 complex / 16 real
@@ -576,7 +564,7 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
 
   for (int rc = rbeg; rc < rend; rc += RCH) {
     const int rn = min(RCH, rend - rc);
-    for (int i = threadIdx.x; i < rn; i += ADJ_THREADS) zs[i] = adj_in<S, CG>(cx, B, rc + i, 0, from_f);
+    for (int i = threadIdx.x; i < rn; i += ADJ_THREADS) zs[i] = adj_in<S>(cx, B, rc + i, 0, from_f);
     if (REAL && (rn & 1) && threadIdx.x == 0) zs[rn] = X::zero();  // pair partner of the last row
     __syncthreads();
     if (cbase < cend) {
@@ -628,7 +616,7 @@ __device__ __forceinline__ void adj_tile(const Ctx &cx, const Tile tl, int from_
   if (tl.start == 0 && sidx == 0 && B.n_skel > 0) {
     for (int i = threadIdx.x; i < B.n_skel; i += ADJ_THREADS) {
       const int q = (B.flags & F_SKEL_IOTA) ? i : cx.idx[B.skel_off + i];
-      static_cast<S *>(cx.part)[B.part_off + q] = adj_in<S, CG>(cx, B, i, 0, from_f);
+      static_cast<S *>(cx.part)[B.part_off + q] = adj_in<S>(cx, B, i, 0, from_f);
     }
   }
   // warp reductions
@@ -693,7 +681,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 7) adj_kernel(const Ctx cx, const
     }
   }
   pdl_wait();
-  adj_tile<S, false>(cx, tl, from_f);
+  adj_tile<S>(cx, tl, from_f);
 }
 
 // ------------------------------------------------------------------------
@@ -1628,7 +1616,7 @@ void mma_dispatch(const Ctx &cx, const Tile *tiles, int ntiles, int from_f, cuda
 // adjoint group sums: dst = sum of the readers' partial ranges (fixed order,
 // no atomics).
 // ------------------------------------------------------------------------
-template <class S, bool CG>
+template <class S>
 __device__ __forceinline__ void reduce_piece(const Ctx &cx, const Piece p, const int64_t *__restrict__ rd, int slice,
                                              int nslices, int tid, int nthr) {
   using X = Tr<S>;
@@ -1640,7 +1628,7 @@ __device__ __forceinline__ void reduce_piece(const Ctx &cx, const Piece p, const
     S s = X::zero();
     for (int q = 0; q < p.rd_count; ++q) {
       const S *a = part + (rd[p.rd_begin + q] + i) * nr + r;
-      s = X::add(s, CG ? X::ldcg(a) : *a);
+      s = X::add(s, *a);
     }
     if (p.dst_src == SRC_C) {
       const int64_t ci = user_c_index(cx, p.dst_off + i);
@@ -1658,141 +1646,9 @@ __global__ void __launch_bounds__(256) reduce_kernel(const Ctx cx, const Piece *
                                                      const int64_t *__restrict__ rd) {
   pdl_trigger();
   pdl_wait();
-  reduce_piece<S, false>(cx, pieces[blockIdx.x], rd, blockIdx.y, gridDim.y, threadIdx.x, blockDim.x);  // y: slices
+  reduce_piece<S>(cx, pieces[blockIdx.x], rd, blockIdx.y, gridDim.y, threadIdx.x, blockDim.x);  // y: slices
 }
 
-
-// ------------------------------------------------------------------------
-// Dataflow nrhs = 1 apply ("flow" kernels): ONE launch walks every phase of a
-// direction (forward: stages 0..L+1; adjoint: the leaf stage, then per stage
-// the unfused group sums and the stage, then the sums into c) with no grid
-// barrier and no per-stage launch, drain or ramp:
-//  * units (the nrhs = 1 tiles and group-sum pieces, phase by phase, LPT
-//    order inside a phase) are dequeued from ONE global counter by resident
-//    128-thread CTAs (7 per SM);
-//  * a CTA first prefetches its unit's factor lines into L2 (the factors never
-//    depend on earlier stages), then waits — once per unit — until the
-//    previous phase's done-counter is complete, then runs the same tile body
-//    as the per-stage kernels (factor streamed by 16-byte register loads,
-//    workspace read through L2), and publishes on its phase's done-counter.
-// The factor stream is register loads from many warps, not a shared-memory
-// ring: a cp.async / TMA ring fed by one producer warp per CTA streamed the
-// strided 1 KB factor-column segments at only 2-4.7 TB/s, register loads from
-// 28 warps per SM at 6.9 TB/s (profiles/r02_tma_stream.txt,
-// r02_ncu_flow_ring_c2.txt).
-// Deadlock freedom: a unit waits only on units of earlier phases, which were
-// dequeued earlier by CTAs that are resident (they executed the dequeue) and
-// that finish a unit before taking the next — by induction on the unit index
-// every unit completes, whatever the grid size or residency.
-// Counters: done[p] per phase, the dequeue counter ctr[nph] and an exit
-// counter ctr[nph + 1]; the last CTA to exit re-arms all of them.
-// ------------------------------------------------------------------------
-constexpr int FL_THREADS = 128;
-constexpr int FL_MINB = 6;      // CTAs per SM the registers are sized for (<= 80: no spills)
-constexpr int FL_MAXPH = 64;
-constexpr int FL_PF_COLS = 128; // factor columns (forward) / column lines (adjoint) prefetched per unit
-
-__device__ __forceinline__ int ld_acquire(const int *p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long ns;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-  return ns;
-}
-
-template <class S, bool ADJ>
-__global__ void __launch_bounds__(FL_THREADS, FL_MINB) flow_kernel(const Ctx cx, const Phase *__restrict__ phases,
-                                                                   int nph, const Tile *__restrict__ tiles,
-                                                                   const Piece *__restrict__ pieces,
-                                                                   const int64_t *__restrict__ rd, int *ctr,
-                                                                   unsigned long long *stamps) {
-  __shared__ Phase sph[FL_MAXPH];
-  __shared__ int sstart[FL_MAXPH + 1];
-  __shared__ int s_u;
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int p = 0; p < nph; ++p) {
-      sph[p] = phases[p];
-      sstart[p] = acc;
-      acc += phases[p].count;
-    }
-    sstart[nph] = acc;
-    if (stamps && blockIdx.x == 0) stamps[0] = globaltimer();
-  }
-  __syncthreads();
-  const int total = sstart[nph];
-  int *done = ctr, *deq = ctr + nph, *exitc = ctr + nph + 1;
-  for (;;) {
-    if (threadIdx.x == 0) s_u = atomicAdd(deq, 1);
-    __syncthreads();
-    const int u = s_u;
-    if (u >= total) break;
-    int p = 0;
-    while (p + 1 < nph && sstart[p + 1] <= u) ++p;
-    const Phase ph = sph[p];
-    const int t = ph.off + (u - sstart[p]);
-    if (ph.kind != PH_SUM) {
-      // L2 prefetch of the unit's factor lines while the dependency resolves
-      const Tile tl = tiles[t];
-      const DevBlock &B = cx.blocks[tl.blk];
-      const char *T = reinterpret_cast<const char *>(static_cast<const S *>(cx.coef) + B.coef_off);
-      if (!ADJ) {
-        // forward: the tile's rows of (up to) FL_PF_COLS columns of its range
-        int jbeg = 0, jend = B.n_red;
-        if (tl.pad >= 0) {
-          const int chunk = ((B.n_red + B.pad - 1) / B.pad + 31) & ~31;
-          jbeg = (tl.pad & 255) * chunk;
-          jend = min(B.n_red, jbeg + chunk);
-        }
-        const int j = jbeg + threadIdx.x;
-        if (j < jend && threadIdx.x < FL_PF_COLS) {
-          const char *col = T + ((int64_t)j * B.ld + tl.start) * (int64_t)sizeof(S);
-          for (int o = 0; o < tl.count * (int)sizeof(S); o += 128) prefetch_l2(col + o);
-        }
-      } else {
-        // adjoint: the first 1 KB of each of the tile's columns (rows of its range)
-        int rbeg = 0;
-        if (tl.pad >= 0) rbeg = (tl.pad & 255) * ((((B.r_out + B.pad2 - 1) / B.pad2) + 31) & ~31);
-        const int col = tl.start + (threadIdx.x >> 3), line = threadIdx.x & 7;
-        if ((threadIdx.x >> 3) < tl.count && line * 128 < (B.r_out - rbeg) * (int)sizeof(S))
-          prefetch_l2(T + ((int64_t)col * B.ld + rbeg) * (int64_t)sizeof(S) + line * 128);
-      }
-    }
-    // the previous phase must be complete (transitively: every earlier one)
-    if (p > 0 && threadIdx.x == 0) {
-      const int need = sph[p - 1].count;
-      const int *dp = done + p - 1;
-      while (ld_acquire(dp) < need) __nanosleep(200);
-    }
-    __syncthreads();
-    if (ph.kind == PH_SUM)
-      reduce_piece<S, true>(cx, pieces[t], rd, 0, 1, threadIdx.x, FL_THREADS);
-    else if (!ADJ)
-      fwd_tile_lat<S, true>(cx, tiles[t]);
-    else
-      adj_tile<S, true>(cx, tiles[t], ph.from_f);
-    // unit complete: publish on the phase's done counter (the barrier orders
-    // every thread's stores before thread 0's fence; the fence is cumulative)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const int old = atomicAdd(done + p, 1);
-      if (stamps && old == ph.count - 1) stamps[p + 1] = globaltimer();
-    }
-  }
-  // this CTA has dequeued for the last time and finished its units: the last
-  // CTA out re-arms the counters for the next apply
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(exitc, 1) == (int)gridDim.x - 1) {
-      for (int q = 0; q < nph + 2; ++q) ctr[q] = 0;
-      __threadfence();
-    }
-  }
-}
 
 constexpr int MAX_GRID_Y = 65535;
 
@@ -1865,38 +1721,6 @@ void launch_repack(const double *src, double *dst, const Repack *jobs, int njobs
     const int nj = njobs - j0 < 65535 ? njobs - j0 : 65535;
     repack_kernel<<<nj, 256, 0, (cudaStream_t)stream>>>(src, dst, jobs + j0);
   }
-}
-
-template <class S>
-int flow_grid_t() {
-  int dev = 0, sms = 0, pf = 0, pa = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, flow_kernel<S, false>, FL_THREADS, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pa, flow_kernel<S, true>, FL_THREADS, 0);
-  return sms * (pf < pa ? pf : pa);
-}
-
-int persist_grid(bool is_complex) { return is_complex ? flow_grid_t<double2>() : flow_grid_t<double>(); }
-
-int launch_persist(bool is_complex, bool adjoint, const Ctx &ctx, const Phase *phases, int nph, const Tile *tiles,
-                   const Piece *pieces, const int64_t *rd, int *ctr, unsigned long long *stamps, int grid,
-                   void *stream) {
-  if (nph <= 0) return 0;
-  if (nph > FL_MAXPH) return (int)cudaErrorInvalidValue;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (is_complex) {
-    if (adjoint)
-      flow_kernel<double2, true><<<grid, FL_THREADS, 0, st>>>(ctx, phases, nph, tiles, pieces, rd, ctr, stamps);
-    else
-      flow_kernel<double2, false><<<grid, FL_THREADS, 0, st>>>(ctx, phases, nph, tiles, pieces, rd, ctr, stamps);
-  } else {
-    if (adjoint)
-      flow_kernel<double, true><<<grid, FL_THREADS, 0, st>>>(ctx, phases, nph, tiles, pieces, rd, ctr, stamps);
-    else
-      flow_kernel<double, false><<<grid, FL_THREADS, 0, st>>>(ctx, phases, nph, tiles, pieces, rd, ctr, stamps);
-  }
-  return (int)cudaGetLastError();
 }
 
 namespace {

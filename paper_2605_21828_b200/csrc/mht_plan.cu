@@ -139,19 +139,6 @@ struct mht_plan {
   int64_t *d_zdel = nullptr;
   unsigned long long **d_peersync = nullptr;
   std::vector<void *> ipc_open;  // peer mappings opened by mht_shard_open_peers
-  // persistent nrhs = 1 apply (one cooperative launch per direction)
-  // off by default: with CUDA-graph replay the per-stage launches measured
-  // faster (profiles/r01_persistent_ab.txt: the cooperative kernel's union
-  // body needs 96-128 registers, 4-5 CTAs/SM, against 7 for the adjoint alone)
-  int persist = 0;              // 1 on (one cooperative launch per direction), 0 per-stage launches
-  int persist_grid = 0;
-  Phase *d_phases = nullptr;
-  Range ph_fwd, ph_adj_fused, ph_adj_unfused;
-  std::vector<Phase> h_phases;
-  int *d_ctr = nullptr;
-  unsigned long long *d_stamps = nullptr;  // per-phase globaltimer stamps (profiling)
-  std::vector<double> last_phase_ms[2];    // [dir] per-phase durations of the last profiled apply
-  bool want_stamps[2] = {false, false};
   int64_t *d_rdtab = nullptr;
   void *d_tmaps = nullptr;    // CUtensorMap per materialised block (complex adjoint TMA tiles)
   bool fused_sum = true;        // adjoint group sums on the consumer's load (MHT_FUSED_SUM=0: off)
@@ -218,7 +205,7 @@ struct mht_plan {
       if (p) cudaFree(p);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (void *p : {(void *)d_coef, (void *)d_idx, (void *)d_perm, (void *)d_permk, (void *)d_blocks, (void *)d_fwd, (void *)d_fwd1, d_fsplit, (void *)d_fcount,
-                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, (void *)d_phases, (void *)d_ctr, (void *)d_stamps, d_msplit, (void *)d_mcount, d_ctmp, d_tmaps, d_z, d_part, d_hc, d_hf})
+                    (void *)d_adj, (void *)d_adjm, (void *)d_pieces, (void *)d_rd, (void *)d_rdtab, d_msplit, (void *)d_mcount, d_ctmp, d_tmaps, d_z, d_part, d_hc, d_hf})
       if (p) cudaFree(p);
   }
 };
@@ -1102,35 +1089,6 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
     }
   }
 
-  // ------------------------------------------------ persistent phases (nrhs = 1)
-  {
-    auto add = [&](int32_t kind, int32_t from_f, Range r, int32_t stage) {
-      if (r.count <= 0) return;
-      Phase ph;
-      memset(&ph, 0, sizeof ph);
-      ph.kind = kind;
-      ph.from_f = from_f;
-      ph.off = r.off;
-      ph.count = r.count;
-      ph.stage = stage;
-      P->h_phases.push_back(ph);
-    };
-    P->ph_fwd.off = (int32_t)P->h_phases.size();
-    for (int s = 0; s < L + 2; ++s) add(PH_FWD, 0, P->fwd1[s], s);
-    P->ph_fwd.count = (int32_t)P->h_phases.size() - P->ph_fwd.off;
-    for (int fused = 1; fused >= 0; --fused) {
-      Range &R = fused ? P->ph_adj_fused : P->ph_adj_unfused;
-      R.off = (int32_t)P->h_phases.size();
-      add(PH_ADJ, 1, P->adj[L + 1], L + 1);
-      for (int s = L; s >= 0; --s) {
-        add(PH_SUM, 0, fused ? P->pieces_u[s] : P->pieces[s], s);
-        add(PH_ADJ, 0, P->adj[s], s);
-      }
-      add(PH_SUM, 0, P->cpieces, -1);
-      R.count = (int32_t)P->h_phases.size() - R.off;
-    }
-  }
-
   // ------------------------------------------------ upload
   mht_status st;
   if ((st = upload(&P->d_idx, idx_all, P->device_bytes)) != MHT_OK) return st;
@@ -1154,17 +1112,6 @@ mht_status load_impl(const char *path, int device, std::unique_ptr<mht_plan> &P,
   if ((st = upload(&P->d_pieces, pieces_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_rd, rd_all, P->device_bytes)) != MHT_OK) return st;
   if ((st = upload(&P->d_rdtab, rdtab, P->device_bytes)) != MHT_OK) return st;
-  if ((st = upload(&P->d_phases, P->h_phases, P->device_bytes)) != MHT_OK) return st;
-  {
-    const int maxph = std::max<int>(1, std::max(P->ph_fwd.count, std::max(P->ph_adj_fused.count, P->ph_adj_unfused.count)));
-    // per-phase done counters + the dequeue and exit counters of the flow kernel
-    CUDA_TRY(cudaMalloc((void **)&P->d_ctr, (size_t)(maxph + 2) * sizeof(int)));
-    CUDA_TRY(cudaMemset(P->d_ctr, 0, (size_t)(maxph + 2) * sizeof(int)));
-    CUDA_TRY(cudaMalloc((void **)&P->d_stamps, (size_t)(maxph + 1) * 2 * sizeof(unsigned long long)));
-    P->device_bytes += (int64_t)maxph * 4 + (maxph + 1) * 16;
-  }
-  P->persist_grid = persist_grid(P->cplx);
-  if (P->persist_grid <= 0) P->persist = 0;
   return MHT_OK;
 }
 
@@ -1257,25 +1204,6 @@ void timed(mht_plan *P, int kind, int stage, int nrhs, int count, F &&launch) {
   P->recs.push_back({kind, stage, nrhs, a, b});
 }
 
-bool use_persist(const mht_plan *P, int nrhs) { return nrhs == 1 && P->persist != 0 && P->shard_G == 1; }
-
-unsigned long long *stamp_buf(mht_plan *P, int dir) {
-  if (!P->prof) return nullptr;
-  P->want_stamps[dir] = true;
-  const int maxph = std::max<int>(1, std::max(P->ph_fwd.count, std::max(P->ph_adj_fused.count, P->ph_adj_unfused.count)));
-  return P->d_stamps + dir * (maxph + 1);
-}
-
-mht_status run_persist(mht_plan *P, const Ctx &cx, Range ph, int dir) {
-  int err = 0;
-  timed(P, dir, -2, 1, 1, [&] {
-    err = launch_persist(P->cplx, dir == 1, cx, P->d_phases + ph.off, ph.count, dir == 1 ? P->d_adj : P->d_fwd1,
-                         P->d_pieces, P->d_rd, P->d_ctr, stamp_buf(P, dir), P->persist_grid, P->stream);
-  });
-  if (err != 0) return fail(MHT_ERR_CUDA, std::string("persistent launch: ") + cudaGetErrorString((cudaError_t)err));
-  return MHT_OK;
-}
-
 // part: 0 the whole apply; sharded plans 1 = stages 0..ls (before the
 // exchange), 2 = stages ls+1..L+1 (after it)
 mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs, int part = 0) {
@@ -1283,12 +1211,6 @@ mht_status run_forward(mht_plan *P, const void *c, void *f, int nrhs, int part =
   cx.c = c;
   cx.fout = f;
   const int s_lo = part == 2 ? P->shard_ls + 1 : 0, s_hi = part == 1 ? P->shard_ls : P->L + 1;
-  if (part == 0 && use_persist(P, nrhs)) {
-    mht_status st = run_persist(P, cx, P->ph_fwd, 0);
-    if (st != MHT_OK) return st;
-    CUDA_TRY(cudaGetLastError());
-    return MHT_OK;
-  }
   unsigned long long *own_sync =
       reinterpret_cast<unsigned long long *>(static_cast<char *>(P->d_z) + P->sync_byte_off);
   if (part == 2 && P->x_on) launch_xwait(own_sync, 0, P->shard_G, P->stream);  // every peer's z_ls stores landed
@@ -1312,12 +1234,6 @@ mht_status run_adjoint(mht_plan *P, const void *f, void *c, int nrhs, int part =
   cx.fin = f;
   cx.cw = c;
   const int L = P->L;
-  if (part == 0 && use_persist(P, nrhs)) {
-    mht_status st = run_persist(P, cx, cx.fused ? P->ph_adj_fused : P->ph_adj_unfused, 1);
-    if (st != MHT_OK) return st;
-    CUDA_TRY(cudaGetLastError());
-    return MHT_OK;
-  }
   auto adj_stage = [&](int s, bool from_f) {
     if (nrhs == 1)
       timed(P, 1, s, nrhs, P->adj[s].count,
@@ -1946,33 +1862,6 @@ mht_status mht_set_fused_sums(mht_plan *P, int on) {
   CUDA_TRY(cudaStreamSynchronize(P->stream));
   P->fused_sum = on != 0;
   P->clear_graphs();
-  return MHT_OK;
-}
-
-mht_status mht_set_persistent(mht_plan *P, int on) {
-  if (!P) return fail(MHT_ERR_INVALID_ARG, "null plan");
-  CUDA_TRY(cudaStreamSynchronize(P->stream));
-  P->persist = (on != 0 && P->persist_grid > 0) ? 1 : 0;
-  P->clear_graphs();
-  return MHT_OK;
-}
-
-mht_status mht_phase_times(mht_plan *P, int dir, double *ms, int32_t *stage, int32_t *kind, int cap, int *nphases) {
-  if (!P || !nphases || dir < 0 || dir > 1) return fail(MHT_ERR_INVALID_ARG, "bad argument");
-  *nphases = 0;
-  if (!P->want_stamps[dir]) return MHT_OK;
-  CUDA_TRY(cudaStreamSynchronize(P->stream));
-  const Range ph = dir == 0 ? P->ph_fwd : (P->fused_sum ? P->ph_adj_fused : P->ph_adj_unfused);
-  const int maxph = std::max<int>(1, std::max(P->ph_fwd.count, std::max(P->ph_adj_fused.count, P->ph_adj_unfused.count)));
-  std::vector<unsigned long long> st(ph.count + 1);
-  CUDA_TRY(cudaMemcpy(st.data(), P->d_stamps + dir * (maxph + 1), st.size() * 8, cudaMemcpyDeviceToHost));
-  const int n = std::min(cap, ph.count);
-  for (int i = 0; i < n; ++i) {
-    if (ms) ms[i] = (double)(st[i + 1] - st[i]) * 1e-6;
-    if (stage) stage[i] = P->h_phases[ph.off + i].stage;
-    if (kind) kind[i] = P->h_phases[ph.off + i].kind;
-  }
-  *nphases = n;
   return MHT_OK;
 }
 

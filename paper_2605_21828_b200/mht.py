@@ -26,7 +26,7 @@ EXPORTED = [
     "mht_plan_load_shard", "mht_shard_info", "mht_shard_workspace", "mht_apply_shard_begin",
     "mht_apply_shard_end", "mht_apply_adjoint_shard_begin", "mht_apply_adjoint_shard_end",
     "mht_shard_export", "mht_shard_open_peers", "mht_shard_set_peers", "mht_shard_close_peers",
-    "mht_set_graphs", "mht_set_fused_sums", "mht_set_persistent", "mht_phase_times", "mht_sync",
+    "mht_set_graphs", "mht_set_fused_sums", "mht_sync",
     "mht_stage_stats", "mht_set_profiling", "mht_profile_get", "mht_profile_reset", "mht_plan_destroy",
     "mht_status_string", "mht_last_error", "mht_build_info",
 ]
@@ -85,9 +85,6 @@ def load_library(path: str = LIB_PATH):
     L.mht_shard_close_peers.argtypes = [vp]
     L.mht_set_graphs.argtypes = [vp, i32]
     L.mht_set_fused_sums.argtypes = [vp, i32]
-    L.mht_set_persistent.argtypes = [vp, i32]
-    L.mht_phase_times.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int32), C.POINTER(C.c_int32), i32,
-                                  C.POINTER(C.c_int32)]
     L.mht_sync.argtypes = [vp]
     L.mht_stage_stats.argtypes = [vp, i32, C.POINTER(i64), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                   C.POINTER(C.c_int32)]
@@ -322,23 +319,6 @@ class Plan:
 
     def set_graphs(self, on: bool):
         _check(load_library().mht_set_graphs(self._h, int(bool(on))), "mht_set_graphs")
-
-    def set_persistent(self, on: bool):
-        """nrhs = 1 applies as ONE dataflow launch per direction (True: the
-        flow kernel, TMA-fed, per-phase done counters) or one launch per stage
-        (False).  Both are deterministic; they sum in different orders."""
-        _check(load_library().mht_set_persistent(self._h, int(bool(on))), "mht_set_persistent")
-
-    def phase_times(self, direction: int):
-        """[(stage, kind, ms)] of the last profiled persistent apply (kind 0
-        forward stage, 1 adjoint stage, 2 group sums; stage -1 = sums into c)."""
-        cap = 4 * (self.L + 3)
-        ms = (C.c_double * cap)()
-        st = (C.c_int32 * cap)()
-        kd = (C.c_int32 * cap)()
-        n = C.c_int32()
-        _check(load_library().mht_phase_times(self._h, direction, ms, st, kd, cap, C.byref(n)), "mht_phase_times")
-        return [(st[i], kd[i], ms[i]) for i in range(n.value)]
 
     def set_fused_sums(self, on: bool):
         """Adjoint group sums on the consumer's load (True, default) or as a

@@ -134,7 +134,7 @@ def test_config1_quadtree_frequency_variant(gpu, oracle_lib, plans):
 def test_frequency_permutation_plan_paths(gpu, oracle_lib, plans):
     """A version-2 plan (perm_k: the quadtree-frequency order, c in the user's
     eigenvalue order, reading A18) through every path that reads or writes c:
-    the nrhs = 1 kernels (per stage and one-launch), the classic and
+    the nrhs = 1 kernels, the classic and
     warp-specialised DMMA kernels, the fused spectral filter on both sides and a
     2-way sharded emulation; all vs O2 element by element and vs the dense sum."""
     from paper_2605_21828_b200 import shard as SH
@@ -145,10 +145,10 @@ def test_frequency_permutation_plan_paths(gpu, oracle_lib, plans):
     P, O = check_plan(gpu, oracle_lib, path, w, (1, 5, 16, 33), dense=flat_dense(oracle_lib, w))
     c, y = mi.complex_gaussian(3, w.m, 7), mi.complex_gaussian(3, w.n, 8)
     ct, yt = torch.from_numpy(c).cuda(), torch.from_numpy(y).cuda()
-    P.set_persistent(True)
+    P.set_graphs(False)
     assert o2_err(P.apply(ct[:1]).cpu().numpy(), O.apply(c[:1])) <= PARITY
     assert o2_err(P.adjoint(yt[:1]).cpu().numpy(), O.adjoint(y[:1])) <= PARITY
-    P.set_persistent(False)
+    P.set_graphs(True)
     F = np.linspace(0.5, 2.0, w.m)
     Ft = torch.from_numpy(F).cuda()
     assert o2_err(P.apply_diag(ct, Ft).cpu().numpy(), O.apply(c * F[None, :])) <= PARITY
@@ -392,54 +392,6 @@ def test_split_k_small_blocks(gpu, oracle_lib, plans):
         assert torch.equal(a1, a2)
         ad = torch.from_numpy(Phi).cuda().T @ y[0]
         assert (torch.linalg.vector_norm(a1[0] - ad) / torch.linalg.vector_norm(ad)).item() < 1e-11
-        P.close()
-
-
-def test_flow_kernel_one_launch_apply(gpu, oracle_lib, plans):
-    """nrhs = 1 applies as ONE dataflow launch per direction (mht_set_persistent:
-    TMA ring of factor chunks, per-phase done counters, no grid barrier) on
-    complex and real plans with aliases and COPY blocks, split tiles, unfused
-    sums, wide blocks (x windows reloaded past 1,024 columns) and tall blocks
-    (z windows past 1,024 rows): element-by-element parity with O2 and with the
-    per-stage launches (different summation order: 1e-12, not bitwise),
-    bitwise repeatability across applies (counters re-armed in-kernel) and
-    identical graph replay."""
-    rng = np.random.default_rng(21)
-    cases = [flat_case(plans, 1024, 32, 4, 1e-15, name="exact"), flat_case(plans, 2048, 32, 4, 1e-8)]
-    Phi = rng.standard_normal((3000, 200))
-    cases.append((_dense_plan(plans, Phi, 1, 1e-12, "persist_tall"), mi.Workload("pt", "mesh", 3000, 200, "float64", 1e-12, 1)))
-    Phi = rng.standard_normal((200, 3000))
-    cases.append((_dense_plan(plans, Phi, 1, 1e-12, "persist_wide"), mi.Workload("pw", "mesh", 200, 3000, "float64", 1e-12, 1)))
-    path_t, w_t = flat_case(plans, 8192, 16, 2, 1e-10, name="tall")
-    cases.append((path_t, w_t))
-    for path, w in cases:
-        P = gpu.Plan(path)
-        O = oracle_lib.Plan(path)
-        if w.dtype == "complex128":
-            c, y = mi.complex_gaussian(1, w.m, 401), mi.complex_gaussian(1, w.n, 402)
-        else:
-            c, y = mi.real_gaussian(1, w.m, 401), mi.real_gaussian(1, w.n, 402)
-        ct, yt = torch.from_numpy(c).cuda(), torch.from_numpy(y).cuda()
-        fo, ao = O.apply(c), O.adjoint(y)
-        res = {}
-        for mode in (True, False):
-            P.set_persistent(mode)
-            for fused in (True, False):
-                P.set_fused_sums(fused)
-                for graphs in (True, False):
-                    P.set_graphs(graphs)
-                    f = [P.apply(ct).cpu() for _ in range(3)]
-                    a = [P.adjoint(yt).cpu() for _ in range(3)]
-                    assert all(torch.equal(f[0], x) for x in f[1:]) and all(torch.equal(a[0], x) for x in a[1:])
-                    res[(mode, fused, graphs)] = (f[0], a[0])
-                    assert o2_err(f[0].numpy(), fo) <= PARITY, (path, mode, fused, graphs)
-                    assert o2_err(a[0].numpy(), ao) <= PARITY, (path, mode, fused, graphs)
-        for k in res:  # one summation order per mode: fused / unfused and graphs are bitwise equal
-            assert torch.equal(res[k][0], res[(k[0], True, True)][0]), (path, k)
-            assert torch.equal(res[k][1], res[(k[0], True, True)][1]), (path, k)
-        P.set_persistent(False)
-        P.set_fused_sums(True)
-        P.set_graphs(True)
         P.close()
 
 

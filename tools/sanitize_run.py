@@ -6,8 +6,7 @@ libmht kernel family on two small plans, one apply of each kind.
 
 Plans: a complex flat plan (n = m = 4096, L = 6, tol 1e-8: c1's shape) and a
 real sphere plan (n = 4096, l <= 63, L = 6, tol 1e-10), built by the CPU
-builder.  Widths: nrhs = 1 (fwd_kernel, adj_kernel, reduce_kernel; also the
-persistent kernel), 17 (mma_kernel), 32 and 40 (mma_ws_kernel for complex,
+builder.  Widths: nrhs = 1 (fwd_kernel, adj_kernel, reduce_kernel), 17 (mma_kernel), 32 and 40 (mma_ws_kernel for complex,
 mma_real_kernel for real; 40 = a partial second RHS chunk).  Graphs off so
 every launch is a plain launch the tool instruments.  Prints one line per case
 with the max relative difference against the nrhs = 1 path (a self-check
@@ -50,16 +49,6 @@ def main():
             ef = (torch.linalg.vector_norm(f[:2] - f1) / torch.linalg.vector_norm(f1)).item()
             ea = (torch.linalg.vector_norm(a[:2] - a1) / torch.linalg.vector_norm(a1)).item()
             print(f"{w.name} nrhs={nrhs}: fwd vs nrhs=1 {ef:.2e}, adj {ea:.2e}", flush=True)
-        if os.environ.get("SAN_PERSIST", "1") == "1":
-            P.set_persistent(True)
-            c = torch.from_numpy(gen(1, w.m, 5)).cuda()
-            y = torch.from_numpy(gen(1, w.n, 6)).cuda()
-            f, a = P.apply(c), P.adjoint(y)
-            torch.cuda.synchronize()
-            P.set_persistent(False)
-            ef = (torch.linalg.vector_norm(f - P.apply(c)) / torch.linalg.vector_norm(f)).item()
-            ea = (torch.linalg.vector_norm(a - P.adjoint(y)) / torch.linalg.vector_norm(a)).item()
-            print(f"{w.name} persistent nrhs=1: vs per-stage {ef:.2e}, adj {ea:.2e}", flush=True)
         P.close()
     print("sanitize_run done", flush=True)
 
