@@ -45,6 +45,30 @@ def test_flat_analysis_equals_fft_on_uniform_grid(oracle_lib, N):
     assert rel(c, ref) < 1e-12
 
 
+def test_flat_synth_equals_fft_at_c2_mode_box(oracle_lib):
+    """SURVEY §8(c) pin at N = 256: the whole [-128, 127]^2 mode box of
+    configs[1] (65,536 modes) on the 256 x 256 uniform grid, against numpy's
+    FFT on 512 seeded grid points (the dense sum over every mode for each;
+    the row subset keeps the CPU suite fast), synthesis and analysis."""
+    N = 256
+    x = mi.grid_points(N)
+    k = mi.flat_modes(N)
+    rows = np.sort(np.random.default_rng(11).choice(N * N, 512, replace=False))
+    c = mi.complex_gaussian(1, N * N, 3)
+    f = oracle_lib.flat_synth(x[rows], k, c)
+    C = np.zeros((1, N, N), complex)
+    C[:, k[:, 0] % N, k[:, 1] % N] = c * ((-1.0) ** (k[:, 0] + k[:, 1]))
+    F = (N * N * np.fft.ifft2(C)).reshape(1, -1)[:, rows]
+    assert rel(f, F) < 1e-12
+    # analysis of f supported on the sampled points: sum over those rows only
+    y = np.zeros((1, N * N), complex)
+    y[:, rows] = mi.complex_gaussian(1, 512, 4)
+    a = oracle_lib.flat_analysis(x[rows], k, y[:, rows])
+    Fh = np.fft.fft2(y.reshape(1, N, N))
+    ref = Fh[:, k[:, 0] % N, k[:, 1] % N] * ((-1.0) ** (k[:, 0] + k[:, 1]))
+    assert rel(a, ref) < 1e-12
+
+
 def test_flat_gram_is_N2_identity_on_alias_free_grid(oracle_lib):
     """Phi^* Phi = N^2 I on the alias-free grid."""
     N = 32
