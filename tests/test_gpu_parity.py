@@ -107,6 +107,27 @@ def test_flat_small_parity(gpu, oracle_lib, plans):
     check_plan(gpu, oracle_lib, path, w, (1, 2, 3, 5, 8, 16, 17, 32, 40), dense=flat_dense(oracle_lib, w))
 
 
+def test_wide_rhs_blocks(gpu, oracle_lib, plans):
+    """Wide right-hand-side blocks: nrhs 129 and 200 (several 32-column RHS
+    chunks per tile plus a ragged last chunk, workspace strides above 128) on a
+    complex flat plan and a real sphere plan, synthesis and analysis, element by
+    element vs O2, plus the split into column blocks applied one by one (the
+    transforms are column-independent; the blocks run other kernels — a single
+    column takes the nrhs = 1 path — so they agree to 1e-12, not bitwise)."""
+    path_c, wc = flat_case(plans, 2048, 32, 4, 1e-8)
+    sp = str(plans / "sph_wide.plan")
+    ws = W.sphere_workload(2048, 31, 4, 1e-10)
+    W.build_workload_plan(ws, sp, workers=8, log=None)
+    for path, w in ((path_c, wc), (sp, ws)):
+        P, O = check_plan(gpu, oracle_lib, path, w, (129, 200))
+        gen = mi.complex_gaussian if w.dtype == "complex128" else mi.real_gaussian
+        c = torch.from_numpy(gen(129, w.m, 71)).cuda()
+        f = P.apply(c)
+        parts = torch.cat([P.apply(c[a:b].contiguous()) for a, b in ((0, 64), (64, 128), (128, 129))])
+        assert o2_err(parts.cpu().numpy(), f.cpu().numpy()) <= PARITY
+        P.close()
+
+
 def test_flat_loose_tolerance_compressed(gpu, oracle_lib, plans):
     path, w = flat_case(plans, 4096, 32, 5, 1e-4)
     P, O = check_plan(gpu, oracle_lib, path, w, (1, 7), dense=flat_dense(oracle_lib, w))
